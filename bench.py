@@ -1,0 +1,382 @@
+#!/usr/bin/env python3
+"""bench.py -- RL-JSDE reconstruction throughput (MP/s) on 1..8 B200s.
+
+Workload (BASELINE.json configs[2], the north-star target): one synthetic 4K frame
+(3840 x 2160 HR, synthetic_image seed 501) under a periodic three-quarter-sampling
+pattern of period 4x4 cells (P = 8 HR px, generate_pattern seed 7), reconstructed
+at the reference defaults (W = 32, B = 4, nu = 200, gamma = 0.5, decay 0.8,
+exponent 2, clip on). One step = one full frame; with N ranks (torchrun, one
+process per GPU) every rank reconstructs its own band of block rows (row bands
+with a 14 px halo, no collective on the data path).
+
+  value  : device-resident frame and output, solve kernel timed with CUDA events
+           on the launching stream, L2 flushed (256 MiB write) between steps,
+           max over ranks -> whole-frame MP / step time
+  e2e    : the public C-ABI call with host buffers (tqsb_reconstruct_band on
+           pinned host memory): H2D of the band's frame rows + solve + D2H of the
+           band's output, host wall clock per step, max over ranks
+  --impl reference : the unmodified reference (oracle/_ref, compiled from the
+           reference sources) on this host's cores, same metric, bounded sample
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+F_BLOCK = 3_723_776  # algorithmic flop per 4x4 block at W=32, nu=200
+METRIC = "megapixels/sec reconstructed (RL-JSDE, 4K frame, period 4x4)"
+
+WORKLOADS = {
+    "4k": dict(rows=2160, cols=3840, seed=501, period=8,
+               name="synthetic 3840x2160 4K image, period 4x4 cells (P=8 px)"),
+    "1mp": dict(rows=1024, cols=1024, seed=401, period=8,
+                name="synthetic 1024x1024 (1 MP) image, period 4x4 cells (P=8 px)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="4k", choices=sorted(WORKLOADS))
+    ap.add_argument("--period", type=int, default=None, help="override P (HR px)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=128,
+                    help="HR rows of the CPU baseline strip")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def workload(args):
+    wl = dict(WORKLOADS[args.workload])
+    if args.period:
+        wl["period"] = args.period
+    return wl
+
+
+def make_inputs(wl):
+    import paper_2205_02646_b200 as tq
+    gt = tq.synthetic_image(wl["rows"], wl["cols"], wl["seed"])
+    pat = tq.generate_pattern(7, wl["period"])
+    frame = tq.simulate_measurement(gt, pat)
+    return gt, pat, frame
+
+
+def band_rows(padM, B, rank, world):
+    nbr = padM // B
+    return rank * nbr // world, (rank + 1) * nbr // world
+
+
+def band_frame_rows(br0, br1, B, W, padM, frame_rows):
+    lead = (W - B) // 2
+    omin = min(max(br0 * B - lead, 0), padM - W)
+    omax = min(max((br1 - 1) * B - lead, 0), padM - W)
+    return min(omin // 2, frame_rows - 1), min(frame_rows, (omax + W - 1) // 2 + 1)
+
+
+# ---------------------------------------------------------------- CPU reference
+def run_reference_sample(wl, sample_rows, steps, warmup):
+    """The unmodified reference on a strip of the workload (rows 0..sample_rows),
+    threads = hardware concurrency, shared kernel cache (warm excluded after the
+    first call, like the reference's own bench, pipeline.cpp:258-329)."""
+    import oracle
+    ref = oracle.Reference()
+    gt = ref.synthetic_image(wl["rows"], wl["cols"], wl["seed"])
+    pat = ref.generate_pattern(7, wl["period"])
+    frame = ref.simulate(gt, pat, wl["period"])
+    strip = np.ascontiguousarray(frame[: sample_rows // 2])
+    mp = strip.shape[0] * 2 * strip.shape[1] * 2 / 1e6
+    cache = ref.new_cache()
+    rates, block_rates = [], []
+    try:
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            _, rep = ref.reconstruct(strip, pat, wl["period"], threads=0, cache=cache)
+            wall = time.perf_counter() - t0
+            if i >= warmup:
+                rates.append(mp / wall)
+                block_rates.append(mp / rep.seconds)
+        threads = rep.threads_used
+    finally:
+        ref.free_cache(cache)
+    return dict(value=statistics.mean(rates), block_phase=statistics.mean(block_rates),
+                cores=threads, isa=ref.isa, mp=mp,
+                sample=f"{strip.shape[0] * 2}x{strip.shape[1] * 2} HR strip (rows 0..{sample_rows})"
+                       f" of the workload frame, {steps} timed calls")
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def main_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    wl = workload(args)
+    r = run_reference_sample(wl, args.cpu_sample_rows, args.steps, args.warmup)
+    line = {
+        "metric": METRIC, "value": round(r["value"], 5), "unit": "MP/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(r["mp"] / r["value"] * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "window": 32, "block": 4, "iterations": 200,
+                   "step_width": 0.5, "period_px": wl["period"], "precision": "double",
+                   "threads": r["cores"], "cpu": cpu_model(), "build": f"g++ -O3 -march=x86-64-{r['isa']}"},
+        "cpu_baseline": {"value": round(r["value"], 5), "unit": "MP/s", "cores": r["cores"],
+                         "kind": "reference", "sample": r["sample"],
+                         "block_phase_value": round(r["block_phase"], 5)},
+        "e2e": {"value": round(r["value"], 5), "unit": "MP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm
+def main_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2205_02646_b200 as tq
+
+    wl = workload(args)
+    cfg = tq.ReconstructionConfig()  # reference defaults, clip on, fp32 product path
+    W, B = cfg.window, cfg.block
+    gt, pat, frame = make_inputs(wl)
+    fr, fc = frame.shape
+    M, N = 2 * fr, 2 * fc
+    padM = -(-M // 4) * 4
+    br0, br1 = band_rows(padM, B, rank, world)
+    f0, f1 = band_frame_rows(br0, br1, B, W, padM, fr)
+    out_r0, out_r1 = br0 * B, min(br1 * B, M)
+
+    peaks = tq.probe_peaks(local)
+    plan = tq.Plan(pat, cfg, devices=[local])
+    stream = torch.cuda.current_stream()
+    d_frame = torch.from_numpy(frame).to(f"cuda:{local}")
+    d_out = torch.empty((out_r1 - out_r0, N), dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    t0 = time.perf_counter()
+    rep0 = plan.reconstruct_device(d_frame.data_ptr(), fr, fc, d_out.data_ptr(),
+                                   stream.cuda_stream, band=(br0, br1))
+    torch.cuda.synchronize()
+    warm_s = time.perf_counter() - t0
+    n_blocks = rep0.blocks_processed
+    for _ in range(args.warmup):
+        plan.reconstruct_device(d_frame.data_ptr(), fr, fc, d_out.data_ptr(), stream.cuda_stream,
+                                band=(br0, br1))
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches = 0
+    for a, b in evs:
+        flush.zero_()                       # L2 flush between steps (outside the events)
+        a.record(stream)
+        r = plan.reconstruct_device(d_frame.data_ptr(), fr, fc, d_out.data_ptr(),
+                                    stream.cuda_stream, band=(br0, br1))
+        b.record(stream)
+        launches += r.gpu_launches
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    mean_ms = statistics.mean(step_ms)
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    nbytes_in = frame.nbytes
+    h_in_ptr = tq.lib.tqsb_host_alloc(nbytes_in)
+    h_out_ptr = tq.lib.tqsb_host_alloc((out_r1 - out_r0) * N * 8)
+    import ctypes
+    h_in = np.ctypeslib.as_array((ctypes.c_double * (fr * fc)).from_address(h_in_ptr)).reshape(fr, fc)
+    h_out = np.ctypeslib.as_array(
+        (ctypes.c_double * ((out_r1 - out_r0) * N)).from_address(h_out_ptr)).reshape(-1, N)
+    h_in[...] = frame
+    for _ in range(max(1, args.warmup)):
+        plan.reconstruct_band(h_in, br0, br1, out=h_out)
+    if world > 1:
+        dist.barrier()
+    e2e_t = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        plan.reconstruct_band(h_in, br0, br1, out=h_out)
+        e2e_t.append(time.perf_counter() - t)
+    if world > 1:
+        dist.barrier()
+    e2e_ms = statistics.mean(e2e_t) * 1e3
+    ok_e2e = bool(np.array_equal(h_out, d_out.cpu().numpy()))
+    h2d = (f1 - f0) * fc * 8
+    d2h = (out_r1 - out_r0) * N * 8
+
+    # ---- max / sum over ranks ----
+    vals = torch.tensor([mean_ms, e2e_ms, float(h2d), float(d2h), float(n_blocks),
+                         float(launches)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        mean_ms, e2e_ms = mx[0].item(), mx[1].item()
+        h2d, d2h, tot_blocks, tot_launch = sm[2].item(), sm[3].item(), sm[4].item(), sm[5].item()
+    else:
+        tot_blocks, tot_launch = float(n_blocks), float(launches)
+    mp = M * N / 1e6
+    value = mp / (mean_ms * 1e-3)
+    e2e_value = mp / (e2e_ms * 1e-3)
+    kernel_tflops = F_BLOCK * n_blocks / (statistics.mean(step_ms) * 1e-3) / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_reference_sample(wl, args.cpu_sample_rows, 2, 1)
+            cpu = {"value": round(r["value"], 5), "unit": "MP/s", "cores": r["cores"],
+                   "kind": "reference", "sample": r["sample"], "cpu": cpu_model()}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "MP/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            t = json.load(open(prof))
+            if t.get("workload") == args.workload and t.get("blocks") == n_blocks:
+                traffic = t.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "MP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": wl["name"], "image_hw": [M, N], "period_px": wl["period"],
+                       "window": W, "block": B, "iterations": cfg.max_iterations,
+                       "step_width": cfg.step_width, "clip": True, "compute": "fp32",
+                       "parallelism": f"row bands x{world}", "blocks": int(tot_blocks),
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "hot_columns": "auto"},
+            "e2e": {"value": round(e2e_value, 3), "unit": "MP/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": round(e2e_ms, 3), "matches_device_output": ok_e2e},
+            "roofline": {"bound": "fp32", "achieved": round(kernel_tflops, 3),
+                         "peak": round(peaks["fp32_tflops"], 2), "unit": "TFLOP/s",
+                         "frac": round(kernel_tflops / peaks["fp32_tflops"], 4),
+                         "traffic": traffic,
+                         "kernel": "k_solve_f32 (fused init/greedy loop/synthesis)",
+                         "algorithmic": f"{F_BLOCK} flop/block x {n_blocks} blocks/launch",
+                         "peak_source": "measured this run: FFMA2 probe (tqsb_probe_peaks); "
+                                        "MEASURED_PEAKS.json has no FP32 figure",
+                         "smem_tbps_measured": round(peaks["smem_tbps"], 2)},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": int(tot_launch),
+            "warm_seconds": round(warm_s, 3),
+            "step_ms_all": [round(x, 4) for x in step_ms],
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/* tqsb.h -- C ABI of the B200-native RL-JSDE reconstruction library (libtqsb.so).
+ *
+ * Drop-in boundary for the reference entry point
+ *     ReconstructionReport tqs::reconstruct(const MeasurementFrame&, const QuadrantPattern&,
+ *                                           const ReconstructionConfig&, KernelCache* = nullptr,
+ *                                           const Image* reference = nullptr);
+ * (/root/reference/proj/include/tqs/pipeline.hpp:45-47, src/pipeline.cpp:62-185).
+ *
+ * A plan (tqsb_plan) plays the role of the reference's external KernelCache
+ * (rljsde.hpp:81-100, pipeline.cpp:110-133): it owns the per-offset-class
+ * tables resident in device memory and reuses them across calls. Plain
+ * pointers and sizes only; no exceptions cross the ABI. Status codes map to the
+ * reference's exception types in include/tqsb/reconstruct.hpp:
+ *   TQSB_EINVAL -> std::invalid_argument   (pipeline.cpp:27-42, 66-67, 74-75, 180-181)
+ *   TQSB_ELOGIC -> std::logic_error         (pipeline.cpp:146-147)
+ *   TQSB_ECUDA / TQSB_ENOMEM / TQSB_ENODEV -> std::runtime_error
+ * The message of the last failure on the calling thread is tqsb_last_error().
+ */
+#ifndef TQSB_H
+#define TQSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TQSB_OK 0
+#define TQSB_EINVAL 1
+#define TQSB_ECUDA 2
+#define TQSB_ENOMEM 3
+#define TQSB_ELOGIC 4
+#define TQSB_ENODEV 5
+
+/* Reference Precision (rljsde.hpp:22): storage precision of the reference's tables. */
+#define TQSB_PRECISION_SINGLE 0
+#define TQSB_PRECISION_DOUBLE 1
+
+/* Device arithmetic of the block loop. FP32 is the product path (tables
+ * accumulated in fp64, stored fp32; loop in fp32 with FFMA2). FP64 is the parity
+ * mode: fp64 tables and loop, reproducing the reference's greedy paths. */
+#define TQSB_COMPUTE_FP32 0
+#define TQSB_COMPUTE_FP64 1
+
+/* Mirrors ReconstructionConfig field for field (pipeline.hpp:17-26), with
+ * SolverOptions (basis.hpp:77-82) and WeightingConfig (basis.hpp:15-18) inlined.
+ * `threads` has no device meaning; the device set is given to tqsb_plan_create. */
+typedef struct tqsb_config {
+    int window;                /* W, default 32 (pipeline.hpp:18) */
+    int block;                 /* B, default 4 (pipeline.hpp:19) */
+    int max_iterations;        /* nu, default 200 (basis.hpp:78) */
+    double step_width;         /* gamma_odc in (0,1], default 0.5 (basis.hpp:79) */
+    double spatial_decay;      /* default 0.8 (basis.hpp:16) */
+    double frequency_exponent; /* default 2.0 (basis.hpp:17) */
+    int precision;             /* TQSB_PRECISION_*, default DOUBLE (pipeline.hpp:22) */
+    int clip_output;           /* default 1 (pipeline.hpp:23) */
+    int threads;               /* accepted and validated (>= 0) like the reference; unused */
+    int compute;               /* TQSB_COMPUTE_*, default FP32 */
+    int hot_columns;           /* shared-memory column cache size; -1 = auto */
+} tqsb_config;
+
+/* Mirrors ReconstructionReport (pipeline.hpp:28-39) minus the output image,
+ * which the caller owns. */
+typedef struct tqsb_report {
+    double seconds;            /* block-phase device time (CUDA events, max over devices) */
+    double warm_seconds;       /* table precompute time of this call */
+    double e2e_seconds;        /* host wall time of the whole call (copies included) */
+    long long blocks_processed;
+    long long classes_total;
+    long long classes_interior;
+    long long classes_created; /* cache misses of this call */
+    long long cache_hits;      /* blocks served from resident tables (reference semantics) */
+    long long cache_misses;
+    double psnr_db;            /* vs reference when supplied; +inf when identical */
+    int has_psnr;
+    int gpu_launches;          /* kernels launched by this call */
+} tqsb_report;
+
+typedef struct tqsb_plan tqsb_plan;
+
+const char* tqsb_last_error(void);
+const char* tqsb_version(void);
+
+/* Fills the reference defaults. */
+void tqsb_config_default(tqsb_config* cfg);
+
+/* validate_config (pipeline.cpp:27-42) without a device: TQSB_OK or TQSB_EINVAL. */
+int tqsb_validate_config(const tqsb_config* cfg, int period);
+
+/* Block/class census of pipeline.cpp:84-106 (host only): out[0] = blocks,
+ * out[1] = classesTotal, out[2] = classesInterior. */
+int tqsb_census(int frame_rows, int frame_cols, const tqsb_config* cfg, int period,
+                long long out[3]);
+
+/* Plan: validates like pipeline.cpp:27-42 and binds the pattern
+ * (opaque = (period/2)^2 quadrant indices, grid.hpp:19-34) to `n_devices`
+ * CUDA devices. Tables are built lazily per offset class on first use and stay
+ * resident (per device, replicated). devices = NULL uses 0..n_devices-1. */
+int tqsb_plan_create(const uint8_t* opaque, int period, const tqsb_config* cfg,
+                     const int* devices, int n_devices, tqsb_plan** out);
+int tqsb_plan_destroy(tqsb_plan* plan);
+
+/* Host-buffer entry point, the drop-in for tqs::reconstruct: frame is
+ * frame_rows x frame_cols float64 row-major (MeasurementFrame, grid.hpp:41-53),
+ * out receives (2*frame_rows) x (2*frame_cols) float64 (Image, image.hpp:10-27).
+ * reference (same shape as out) may be NULL; rep may be NULL. Work is split
+ * across the plan's devices in block-row bands. */
+int tqsb_reconstruct(tqsb_plan* plan, const double* frame, int frame_rows, int frame_cols,
+                     double* out, const double* reference, tqsb_report* rep);
+
+/* Band form (one process per GPU): reconstruct only output block rows
+ * [block_row_begin, block_row_end) of the padded image on the plan's first
+ * device. frame is the FULL host frame (only the rows the band's windows need,
+ * halo included, are read); out_band receives rows
+ * [block_row_begin*B, min(block_row_end*B, 2*frame_rows)) x (2*frame_cols). */
+int tqsb_reconstruct_band(tqsb_plan* plan, const double* frame, int frame_rows, int frame_cols,
+                          int block_row_begin, int block_row_end, double* out_band,
+                          tqsb_report* rep);
+
+/* Device-resident form on the plan's first device: d_frame / d_out are device
+ * pointers (same layouts as tqsb_reconstruct), stream a cudaStream_t (NULL =
+ * legacy default). Asynchronous: returns after enqueueing; rep->seconds is 0.
+ * Tables for the frame's classes must be resident (tqsb_plan_warm) or are
+ * built synchronously first. */
+int tqsb_reconstruct_device(tqsb_plan* plan, const double* d_frame, int frame_rows,
+                            int frame_cols, double* d_out, void* stream, tqsb_report* rep);
+
+/* Band form of the device-resident entry point (rows as tqsb_reconstruct_band;
+ * d_frame is the full frame in device memory, d_out_band the band). */
+int tqsb_reconstruct_band_device(tqsb_plan* plan, const double* d_frame, int frame_rows,
+                                 int frame_cols, int block_row_begin, int block_row_end,
+                                 double* d_out_band, void* stream, tqsb_report* rep);
+
+/* Build (if missing) the tables of every class a frame of this size touches,
+ * on every device of the plan (the reference's serial warm pass,
+ * pipeline.cpp:127-133). warm_seconds may be NULL. */
+int tqsb_plan_warm(tqsb_plan* plan, int frame_rows, int frame_cols, double* warm_seconds);
+
+/* Resident table classes and their device bytes (all devices' copies of one device). */
+int tqsb_plan_stats(const tqsb_plan* plan, long long* classes, long long* device_bytes);
+
+/* Table export for parity tests (KernelSet planes, rljsde.hpp:34-52): the
+ * tables of the class of window origin (origin_row, origin_col), built on the
+ * plan's first device, copied to host as fp64: b (K*L complex, k-major [k*L+m]),
+ * c (K*K complex, column-major [uk*K+sk]), d (K). Pass NULL b to query L. */
+int tqsb_plan_export_tables(tqsb_plan* plan, int origin_row, int origin_col, int* local_out,
+                            double* b_re, double* b_im, double* c_re, double* c_im, double* d);
+
+/* Greedy path of one block on the device (parity diagnostics, the analogue of
+ * rljsde_block's IterationHook, rljsde.hpp:75-77): y_local (L values, the
+ * gather_local_values order) for a window at (origin_row, origin_col); picks
+ * receive chosen flat indices, gd the scaled deltas (re, im interleaved),
+ * window_out (optional) the full W*W synthesis. Returns iterations completed
+ * through *n_out. Uses the plan's compute mode. */
+int tqsb_plan_block_trace(tqsb_plan* plan, int origin_row, int origin_col, const double* y_local,
+                          int* picks, double* gd, double* window_out, int* n_out);
+
+/* Host helpers (test support / input side; no device needed). */
+/* generate_pattern (grid.cpp:8-26): mt19937_64, low two bits per cell. */
+int tqsb_generate_pattern(uint64_t seed, int period, int block, uint8_t* opaque_out);
+/* simulate_measurement (grid.cpp:46-66): image rows x cols (even) -> frame. */
+int tqsb_simulate(const double* image, int rows, int cols, const uint8_t* opaque, int period,
+                  double* frame_out);
+/* synthetic test image (tests/support/synthetic.cpp:9-80), values in [0.02, 0.98]. */
+int tqsb_synthetic_image(int rows, int cols, uint64_t seed, double* out);
+/* psnr (pipeline.cpp:221-233): +inf when identical. */
+double tqsb_psnr(const double* reference, const double* estimate, long long n);
+
+/* Pinned host memory for zero-staging transfers (cudaHostAlloc). */
+void* tqsb_host_alloc(size_t bytes);
+void tqsb_host_free(void* p);
+int tqsb_device_count(void);
+
+/* Diagnostics: measured roofline denominators of `device` -- FP32 pipe peak
+ * (FFMA2 chains, TFLOP/s) and shared-memory load bandwidth (LDS.128, TB/s). */
+int tqsb_probe_peaks(int device, double* fp32_tflops, double* smem_tbps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQSB_H */

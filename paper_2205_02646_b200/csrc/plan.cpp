@@ -1,0 +1,1142 @@
+// plan.cpp -- host side of libtqsb: the C ABI (include/tqsb/tqsb.h), validation,
+// block enumeration and class census, the device-resident table store (the
+// KernelCache analogue) and multi-device row-band dispatch.
+//
+// Reference correspondences (/root/reference/proj/...):
+//   validate             src/pipeline.cpp:27-42 (+ frame checks 66-67, 74-75)
+//   enumerate_blocks     src/pipeline.cpp:84-106, offset_class src/rljsde.cpp:12-17
+//   local_system         src/grid.cpp:31-42, 70-102; spatial_weight src/basis.cpp:75-80
+//   frequency weights    src/basis.cpp:90-106; unit table src/basis.cpp:15-26
+//   table store / warm   include/tqs/rljsde.hpp:81-100, src/pipeline.cpp:110-133
+//   report counters      src/pipeline.cpp:168-184; psnr src/pipeline.cpp:221-233
+// The per-block solve, synthesis and placement run on the device (solve_f32.cu,
+// solve_f64.cu); the tables are built on the device (tables.cu). There is no CPU
+// fallback: without a CUDA device every compute entry point fails with TQSB_ENODEV.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/tqsb/tqsb.h"
+#include "tqsb_internal.hpp"
+
+using namespace tqsb;
+
+namespace {
+
+thread_local std::string g_error;
+
+int set_error(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return set_error(_e == cudaErrorMemoryAllocation ? TQSB_ENOMEM : TQSB_ECUDA,       \
+                             std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+    } while (0)
+
+#define TQSB_TRY(expr)            \
+    do {                          \
+        int _rc = (expr);         \
+        if (_rc != TQSB_OK) return _rc; \
+    } while (0)
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// validation: the reference's messages, pipeline.cpp:27-42
+// ---------------------------------------------------------------------------
+int validate(const tqsb_config& c, int period) {
+    if (c.window < 2 || c.window % 2 != 0)
+        return set_error(TQSB_EINVAL, "window size must be even and >= 2");
+    if (c.block < 1 || c.window % c.block != 0)
+        return set_error(TQSB_EINVAL, "block size must divide the window size");
+    if ((c.window - c.block) % 2 != 0)
+        return set_error(TQSB_EINVAL, "window/block sizes must center the target block");
+    if (period <= 0 || period % c.block != 0)
+        return set_error(TQSB_EINVAL, "block size must divide the pattern period");
+    if (c.max_iterations < 0) return set_error(TQSB_EINVAL, "iteration count must be non-negative");
+    if (!(c.step_width > 0.0 && c.step_width <= 1.0))
+        return set_error(TQSB_EINVAL, "step width must lie in (0,1]");
+    if (c.threads < 0) return set_error(TQSB_EINVAL, "thread count must be non-negative");
+    if (c.compute != TQSB_COMPUTE_FP32 && c.compute != TQSB_COMPUTE_FP64)
+        return set_error(TQSB_EINVAL, "unknown compute mode");
+    if (c.precision != TQSB_PRECISION_SINGLE && c.precision != TQSB_PRECISION_DOUBLE)
+        return set_error(TQSB_EINVAL, "unknown precision");
+    return TQSB_OK;
+}
+
+// device-path limits (not in the reference): one warp spans a window row/col
+int validate_device_limits(const tqsb_config& c) {
+    if (c.window > kMaxWindow)
+        return set_error(TQSB_EINVAL, "window sizes above 32 are not supported by the device solver");
+    if (c.compute == TQSB_COMPUTE_FP32 && c.block * c.block > 256)
+        return set_error(TQSB_EINVAL, "block sizes above 16 require compute=fp64");
+    return TQSB_OK;
+}
+
+struct Geometry {
+    int M, N, padM, padN, lead, B, W;
+};
+
+int geometry(const tqsb_config& c, int frame_rows, int frame_cols, Geometry* g) {
+    if (frame_rows < 1 || frame_cols < 1) return set_error(TQSB_EINVAL, "empty measurement frame");
+    g->W = c.window;
+    g->B = c.block;
+    g->M = 2 * frame_rows;
+    g->N = 2 * frame_cols;
+    const int step = std::lcm(c.block, 2);
+    g->padM = round_up(g->M, step);
+    g->padN = round_up(g->N, step);
+    if (g->padM < c.window || g->padN < c.window)
+        return set_error(TQSB_EINVAL, "image is smaller than the model window");
+    g->lead = (c.window - c.block) / 2;
+    return TQSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// block enumeration (pipeline.cpp:84-106)
+// ---------------------------------------------------------------------------
+struct Enumerated {
+    std::vector<Task> tasks;          // row-major order
+    std::vector<int> keys;            // class key per task (row*P + col)
+    std::vector<int> class_order;     // distinct keys in first-seen order
+    std::map<int, std::pair<int, int>> representative;
+    long long classes_total = 0, classes_interior = 0;
+};
+
+void enumerate(const Geometry& g, int period, int br_begin, int br_end, Enumerated* e) {
+    std::vector<char> seen(size_t(period) * period, 0), seen_int(size_t(period) * period, 0);
+    for (int bri = br_begin; bri < br_end; ++bri) {
+        const int br = bri * g.B;
+        for (int bc = 0; bc + g.B <= g.padN; bc += g.B) {
+            const int wr = br - g.lead, wc = bc - g.lead;
+            const int orow = std::clamp(wr, 0, g.padM - g.W), ocol = std::clamp(wc, 0, g.padN - g.W);
+            const bool interior = orow == wr && ocol == wc;
+            const int key = (orow % period) * period + (ocol % period);
+            if (!seen[key]) {
+                seen[key] = 1;
+                ++e->classes_total;
+                e->class_order.push_back(key);
+                e->representative.emplace(key, std::make_pair(orow, ocol));
+            }
+            if (interior && !seen_int[key]) {
+                seen_int[key] = 1;
+                ++e->classes_interior;
+            }
+            e->tasks.push_back(Task{br, bc, orow, ocol});
+            e->keys.push_back(key);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// local measurement system of a window (grid.cpp:31-42, 70-102) and weights
+// ---------------------------------------------------------------------------
+struct LocalSystem {
+    int L = 0;
+    std::vector<signed char> px;   // L*6
+    std::vector<double> w;         // L
+    std::vector<float> mask32;     // W*W
+};
+
+LocalSystem local_system(const std::vector<uint8_t>& opaque, int period, int orow, int ocol,
+                         const tqsb_config& c) {
+    LocalSystem s;
+    const int W = c.window, pc = period / 2;
+    const int r0 = (orow + 1) / 2, r1 = (orow + W - 2) / 2;
+    const int c0 = (ocol + 1) / 2, c1 = (ocol + W - 2) / 2;
+    s.mask32.assign(size_t(W) * W, 0.f);
+    const double center = (W - 1) / 2.0;
+    for (int r = r0; r <= r1; ++r)
+        for (int cc = c0; cc <= c1; ++cc) {
+            const int ce = 2 * r - orow, cg = 2 * cc - ocol;
+            const int q = opaque[size_t(((r % pc) + pc) % pc) * pc + ((cc % pc) + pc) % pc];
+            const double dr = (ce + 0.5) - center, dc = (cg + 0.5) - center;
+            const double w = std::pow(c.spatial_decay, std::sqrt(dr * dr + dc * dc));
+            s.w.push_back(w);
+            for (int quad = 0; quad < 4; ++quad) {  // transparent quadrants, row-major
+                if (quad == q) continue;
+                const int eta = ce + quad / 2, gam = cg + quad % 2;
+                s.px.push_back(static_cast<signed char>(eta));
+                s.px.push_back(static_cast<signed char>(gam));
+                s.mask32[size_t(eta) * W + gam] = float(w * (1.0 / 3.0));
+            }
+            ++s.L;
+        }
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// window constants: unit table, q, rank permutation
+// ---------------------------------------------------------------------------
+struct WindowTables {
+    int W = 0, K = 0, NS = 0, K_pad = 0;
+    std::vector<double> unit64;  // 2W
+    std::vector<float> unit32;   // 2W
+    std::vector<double> q;       // K
+    std::vector<int> perm, src;  // K_pad
+};
+
+WindowTables window_tables(const tqsb_config& c) {
+    WindowTables t;
+    const int W = c.window;
+    t.W = W;
+    t.K = W * W;
+    const int ns = (t.K + 63) / 64;
+    t.NS = ns <= 1 ? 1 : ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 8 ? 8 : 16;
+    t.K_pad = 64 * t.NS;
+    t.unit64.assign(2 * W, 0.0);
+    t.unit64[0] = 1.0;
+    t.unit64[2 * (W / 2)] = -1.0;
+    for (int k = 1; k < W / 2; ++k) {  // FourierTable (basis.cpp:15-26)
+        const double a = 2.0 * 3.14159265358979323846 * k / W;
+        t.unit64[2 * k] = std::cos(a);
+        t.unit64[2 * k + 1] = std::sin(a);
+        t.unit64[2 * (W - k)] = t.unit64[2 * k];
+        t.unit64[2 * (W - k) + 1] = -t.unit64[2 * k + 1];
+    }
+    t.unit32.resize(2 * W);
+    for (int i = 0; i < 2 * W; ++i) t.unit32[i] = float(t.unit64[i]);
+    t.q.resize(t.K);
+    const int half = W / 2;
+    std::vector<std::pair<int, int>> order;
+    for (int s = 0; s < W; ++s)
+        for (int r = 0; r < W; ++r) {  // frequency_weight (basis.cpp:90-97)
+            const int cs = s <= half ? s : W - s, cr = r <= half ? r : W - r;
+            const double radius = std::sqrt(double(cs) * cs + double(cr) * cr);
+            const double maxr = 1.41421356237309504880 * half * (1.0 + 1e-6);
+            t.q[s * W + r] = std::pow(1.0 - radius / maxr, c.frequency_exponent);
+            order.emplace_back(cs * cs + cr * cr, s * W + r);
+        }
+    std::sort(order.begin(), order.end());
+    t.perm.assign(t.K_pad, -1);
+    t.src.assign(t.K_pad, 0);
+    for (int r = 0; r < t.K; ++r) {
+        const int k = order[r].second, s = k / W, rho = k % W;
+        t.perm[r] = k;
+        // half-spectrum source: rows sigma <= W/2, with the self-conjugate rows
+        // 0 and W/2 taking rho > W/2 from their mirror
+        const bool direct = s < half || ((s == 0 || s == half) && rho <= half);
+        if (direct)
+            t.src[r] = s * W + rho;
+        else
+            t.src[r] = (((W - s) % W) * W + (W - rho) % W) | (1 << 30);
+    }
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// per-device state
+// ---------------------------------------------------------------------------
+struct ClassSlab {
+    void* base = nullptr;
+    size_t bytes = 0;
+};
+
+struct WorkKey {
+    int rows, cols, br0, br1;
+    bool operator<(const WorkKey& o) const {
+        return std::tie(rows, cols, br0, br1) < std::tie(o.rows, o.cols, o.br0, o.br1);
+    }
+};
+
+struct Work {
+    Task* d_tasks = nullptr;
+    WorkItem* d_items = nullptr;
+    int n_tasks = 0, n_items = 0;
+    int frame_row0 = 0, frame_row1 = 0;  // frame rows the band needs
+    std::vector<int> keys;                // classes used
+    long long classes_total = 0, classes_interior = 0;
+};
+
+struct Device {
+    int id = 0;
+    int num_sms = 0;
+    int hot = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int* d_perm = nullptr;
+    int* d_src = nullptr;
+    float* d_unit32 = nullptr;
+    double* d_unit64 = nullptr;
+    double* d_q64 = nullptr;
+    std::map<int, int> slot_of;    // class key -> slot
+    std::vector<ClassTab> tabs;    // host mirror
+    std::vector<ClassSlab> slabs;
+    ClassTab* d_tabs = nullptr;
+    size_t d_tabs_cap = 0;
+    std::map<WorkKey, Work> works;
+    double* d_frame = nullptr;
+    size_t frame_cap = 0;
+    double* d_out = nullptr;
+    size_t out_cap = 0;
+    double* h_in = nullptr;   // pinned staging
+    size_t h_in_cap = 0;
+    double* h_out = nullptr;
+    size_t h_out_cap = 0;
+    size_t table_bytes = 0;
+};
+
+} // namespace
+
+struct tqsb_plan {
+    tqsb_config cfg;
+    int period = 0;
+    std::vector<uint8_t> opaque;
+    WindowTables wt;
+    std::vector<std::unique_ptr<Device>> devs;
+    std::mutex mu;
+};
+
+namespace {
+
+int device_init(tqsb_plan* p, Device* d) {
+    CUDA_TRY(cudaSetDevice(d->id));
+    CUDA_TRY(cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, d->id));
+    CUDA_TRY(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreate(&d->ev0));
+    CUDA_TRY(cudaEventCreate(&d->ev1));
+    const WindowTables& t = p->wt;
+    CUDA_TRY(cudaMalloc(&d->d_perm, sizeof(int) * t.K_pad));
+    CUDA_TRY(cudaMalloc(&d->d_src, sizeof(int) * t.K_pad));
+    CUDA_TRY(cudaMalloc(&d->d_unit32, sizeof(float) * 2 * t.W));
+    CUDA_TRY(cudaMalloc(&d->d_unit64, sizeof(double) * 2 * t.W));
+    CUDA_TRY(cudaMalloc(&d->d_q64, sizeof(double) * t.K));
+    CUDA_TRY(cudaMemcpy(d->d_perm, t.perm.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d->d_src, t.src.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d->d_unit32, t.unit32.data(), sizeof(float) * 2 * t.W, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d->d_unit64, t.unit64.data(), sizeof(double) * 2 * t.W, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d->d_q64, t.q.data(), sizeof(double) * t.K, cudaMemcpyHostToDevice));
+    const int maxhot = solve_f32_max_hot(t.NS, d->id);
+    const int K_pad = t.K_pad;
+    int hot = p->cfg.hot_columns < 0 ? maxhot : std::min(p->cfg.hot_columns, maxhot);
+    d->hot = std::clamp(hot, 0, K_pad);
+    return TQSB_OK;
+}
+
+void device_free(Device* d) {
+    if (!d) return;
+    cudaSetDevice(d->id);
+    for (auto& s : d->slabs) cudaFree(s.base);
+    for (auto& kv : d->works) {
+        cudaFree(kv.second.d_tasks);
+        cudaFree(kv.second.d_items);
+    }
+    cudaFree(d->d_tabs);
+    cudaFree(d->d_perm);
+    cudaFree(d->d_src);
+    cudaFree(d->d_unit32);
+    cudaFree(d->d_unit64);
+    cudaFree(d->d_q64);
+    cudaFree(d->d_frame);
+    cudaFree(d->d_out);
+    if (d->h_in) cudaFreeHost(d->h_in);
+    if (d->h_out) cudaFreeHost(d->h_out);
+    if (d->ev0) cudaEventDestroy(d->ev0);
+    if (d->ev1) cudaEventDestroy(d->ev1);
+    if (d->stream) cudaStreamDestroy(d->stream);
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Build the tables of every class in `keys` that is not resident on device d
+// (batched; the serial warm pass of pipeline.cpp:127-133). Returns the number of
+// classes created through *created.
+int ensure_classes(tqsb_plan* p, Device* d, const std::vector<int>& keys,
+                   const std::map<int, std::pair<int, int>>& rep, int* created, int* launches) {
+    std::vector<int> missing;
+    for (int k : keys)
+        if (!d->slot_of.count(k)) missing.push_back(k);
+    *created = int(missing.size());
+    if (missing.empty()) return TQSB_OK;
+    CUDA_TRY(cudaSetDevice(d->id));
+    const WindowTables& t = p->wt;
+    const size_t K = t.K, K_pad = t.K_pad, W = t.W;
+    const bool f32 = true;  // fp32 tables are always built (fp64 planes are kept too)
+    std::vector<ClassBuild> descs;
+    int max_local = 1;
+    for (int key : missing) {
+        const auto [orow, ocol] = rep.at(key);
+        LocalSystem ls = local_system(p->opaque, p->period, orow, ocol, p->cfg);
+        const size_t L = ls.L;
+        max_local = std::max<int>(max_local, int(L));
+        // slab layout
+        size_t off = 0;
+        auto take = [&](size_t bytes) {
+            size_t o = off;
+            off = align_up(off + bytes, 256);
+            return o;
+        };
+        const size_t o_c64 = take(K * K * 2 * 8), o_b64 = take(K * L * 2 * 8),
+                     o_t64 = take(K * L * 2 * 8), o_d64 = take(K * 8),
+                     o_cpack = take(f32 ? K_pad * K_pad * 8 : 0), o_scale = take(K_pad * 4),
+                     o_fac = take(K_pad * 4), o_mask = take(W * W * 4), o_px = take(L * 6 + 8),
+                     o_w = take(L * 8 + 8);
+        ClassSlab slab;
+        slab.bytes = off;
+        CUDA_TRY(cudaMalloc(&slab.base, slab.bytes));
+        char* b = static_cast<char*>(slab.base);
+        CUDA_TRY(cudaMemcpyAsync(b + o_px, ls.px.data(), L * 6, cudaMemcpyHostToDevice, d->stream));
+        CUDA_TRY(cudaMemcpyAsync(b + o_w, ls.w.data(), L * 8, cudaMemcpyHostToDevice, d->stream));
+        CUDA_TRY(cudaMemcpyAsync(b + o_mask, ls.mask32.data(), W * W * 4, cudaMemcpyHostToDevice,
+                                 d->stream));
+        CUDA_TRY(cudaStreamSynchronize(d->stream));  // host vectors die at scope end
+        ClassBuild cb{};
+        cb.local = int(L);
+        cb.px = reinterpret_cast<const signed char*>(b + o_px);
+        cb.w = reinterpret_cast<const double*>(b + o_w);
+        cb.t64 = reinterpret_cast<double*>(b + o_t64);
+        cb.b64 = reinterpret_cast<double*>(b + o_b64);
+        cb.c64 = reinterpret_cast<double*>(b + o_c64);
+        cb.d64 = reinterpret_cast<double*>(b + o_d64);
+        cb.cpack = f32 ? reinterpret_cast<float*>(b + o_cpack) : nullptr;
+        cb.scale = reinterpret_cast<float*>(b + o_scale);
+        cb.fac = reinterpret_cast<float*>(b + o_fac);
+        descs.push_back(cb);
+        ClassTab tab{};
+        tab.cpack = cb.cpack;
+        tab.scale = cb.scale;
+        tab.fac = cb.fac;
+        tab.mask32 = reinterpret_cast<const float*>(b + o_mask);
+        tab.b64 = cb.b64;
+        tab.c64 = cb.c64;
+        tab.d64 = cb.d64;
+        tab.cells = nullptr;
+        tab.local = int(L);
+        d->slot_of[key] = int(d->tabs.size());
+        d->tabs.push_back(tab);
+        d->slabs.push_back(slab);
+        d->table_bytes += slab.bytes;
+    }
+    int rc = launch_tables_batch(descs.data(), int(descs.size()), int(W), int(K_pad),
+                                 p->cfg.step_width, d->d_unit64, d->d_q64, d->d_perm, max_local,
+                                 d->stream, launches);
+    if (rc != 0) return set_error(TQSB_ECUDA, std::string("table build: ") +
+                                                  cudaGetErrorString(cudaError_t(rc)));
+    // refresh the device ClassTab array
+    if (d->tabs.size() > d->d_tabs_cap) {
+        CUDA_TRY(cudaStreamSynchronize(d->stream));
+        cudaFree(d->d_tabs);
+        d->d_tabs_cap = std::max<size_t>(d->tabs.size() * 2, 16);
+        CUDA_TRY(cudaMalloc(&d->d_tabs, sizeof(ClassTab) * d->d_tabs_cap));
+    }
+    CUDA_TRY(cudaMemcpyAsync(d->d_tabs, d->tabs.data(), sizeof(ClassTab) * d->tabs.size(),
+                             cudaMemcpyHostToDevice, d->stream));
+    CUDA_TRY(cudaStreamSynchronize(d->stream));
+    return TQSB_OK;
+}
+
+// Class-sorted tasks and CTA work items for a band of block rows on device d;
+// the band's classes are made resident first (cached per frame shape and band).
+int prepare_band(tqsb_plan* p, Device* d, const Geometry& g, int frame_rows, int frame_cols,
+                 int br0, int br1, Work** out, int* created, int* launches) {
+    *created = 0;
+    const WorkKey wkey{frame_rows, frame_cols, br0, br1};
+    auto it = d->works.find(wkey);
+    if (it != d->works.end()) {
+        *out = &it->second;
+        return TQSB_OK;
+    }
+    Enumerated e;
+    enumerate(g, p->period, br0, br1, &e);
+    TQSB_TRY(ensure_classes(p, d, e.class_order, e.representative, created, launches));
+    Work w;
+    w.keys = e.class_order;
+    w.classes_total = e.classes_total;
+    w.classes_interior = e.classes_interior;
+    w.n_tasks = int(e.tasks.size());
+    int omin = std::numeric_limits<int>::max(), omax = 0;
+    for (const Task& t : e.tasks) {
+        omin = std::min(omin, t.origin_row);
+        omax = std::max(omax, t.origin_row);
+    }
+    if (e.tasks.empty()) omin = omax = 0;
+    w.frame_row0 = std::min(omin / 2, frame_rows - 1);
+    w.frame_row1 = std::min(frame_rows, (omax + g.W - 1) / 2 + 1);
+    // class-sorted (stable) task list, cut into CTA work items of one class each
+    std::vector<std::vector<Task>> by_key(size_t(p->period) * p->period);
+    for (size_t i = 0; i < e.tasks.size(); ++i) by_key[e.keys[i]].push_back(e.tasks[i]);
+    std::vector<Task> sorted;
+    std::vector<WorkItem> items;
+    sorted.reserve(e.tasks.size());
+    const int chunk = (p->cfg.compute == TQSB_COMPUTE_FP32 ? kWarpsF32 : kWarpsF64) * 4;
+    for (int k : e.class_order) {
+        const auto& v = by_key[k];
+        for (size_t s = 0; s < v.size(); s += chunk) {
+            WorkItem wi{};
+            wi.cls = d->slot_of.at(k);
+            wi.start = int(sorted.size() + s);
+            wi.count = int(std::min<size_t>(chunk, v.size() - s));
+            items.push_back(wi);
+        }
+        sorted.insert(sorted.end(), v.begin(), v.end());
+    }
+    w.n_items = int(items.size());
+    (void)frame_cols;
+    CUDA_TRY(cudaSetDevice(d->id));
+    CUDA_TRY(cudaMalloc(&w.d_tasks, sizeof(Task) * std::max<size_t>(1, sorted.size())));
+    CUDA_TRY(cudaMalloc(&w.d_items, sizeof(WorkItem) * std::max<size_t>(1, items.size())));
+    CUDA_TRY(cudaMemcpy(w.d_tasks, sorted.data(), sizeof(Task) * sorted.size(),
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(w.d_items, items.data(), sizeof(WorkItem) * items.size(),
+                        cudaMemcpyHostToDevice));
+    auto ins = d->works.emplace(wkey, std::move(w));
+    *out = &ins.first->second;
+    return TQSB_OK;
+}
+
+int ensure_buffer(double** buf, size_t* cap, size_t n) {
+    if (*cap >= n) return TQSB_OK;
+    cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    CUDA_TRY(cudaMalloc(buf, sizeof(double) * std::max<size_t>(n, 1)));
+    *cap = n;
+    return TQSB_OK;
+}
+
+int ensure_pinned(double** buf, size_t* cap, size_t n) {
+    if (*cap >= n) return TQSB_OK;
+    if (*buf) cudaFreeHost(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(buf), sizeof(double) * std::max<size_t>(n, 1),
+                           cudaHostAllocDefault));
+    *cap = n;
+    return TQSB_OK;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+SolveArgs base_args(tqsb_plan* p, Device* d) {
+    SolveArgs a{};
+    a.tabs = d->d_tabs;
+    a.wc.perm = d->d_perm;
+    a.wc.src = d->d_src;
+    a.wc.unit32 = d->d_unit32;
+    a.wc.unit64 = d->d_unit64;
+    a.wc.q64 = d->d_q64;
+    a.window = p->cfg.window;
+    a.block = p->cfg.block;
+    a.iterations = p->cfg.max_iterations;
+    a.step = p->cfg.step_width;
+    a.clip = p->cfg.clip_output;
+    a.hot = d->hot;
+    return a;
+}
+
+int launch(tqsb_plan* p, Device* d, const SolveArgs& a, cudaStream_t s) {
+    int rc = p->cfg.compute == TQSB_COMPUTE_FP32
+                 ? launch_solve_f32(a, p->wt.NS, s, d->num_sms)
+                 : launch_solve_f64(a, s, d->num_sms);
+    if (rc != 0)
+        return set_error(TQSB_ECUDA, std::string("solve launch: ") +
+                                         cudaGetErrorString(cudaError_t(rc)));
+    return TQSB_OK;
+}
+
+struct BandResult {
+    int rc = TQSB_OK;
+    std::string err;
+    float ms = 0.f;
+    double warm = 0.0;
+    int created = 0;
+    int launches = 0;
+    long long classes_total = 0, classes_interior = 0, blocks = 0;
+};
+
+// Host-buffer band run on device d: H2D of the band's frame rows (pinned
+// staging), solve, D2H of the band's output rows.
+void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* frame,
+                   int frame_rows, int frame_cols, int br0, int br1, double* out_band,
+                   BandResult* r) {
+    auto fail = [&](int rc) {
+        r->rc = rc;
+        r->err = g_error;
+    };
+    if (cudaSetDevice(d->id) != cudaSuccess) return fail(set_error(TQSB_ECUDA, "cudaSetDevice"));
+    Work* w = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    int rc = prepare_band(p, d, g, frame_rows, frame_cols, br0, br1, &w, &r->created, &r->launches);
+    if (rc) return fail(rc);
+    r->warm = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r->classes_total = w->classes_total;
+    r->classes_interior = w->classes_interior;
+    r->blocks = w->n_tasks;
+    const int fr0 = w->frame_row0, fr1 = w->frame_row1;
+    const size_t in_n = size_t(fr1 - fr0) * frame_cols;
+    const int orow0 = br0 * g.B, orow1 = std::min(br1 * g.B, g.M);
+    const size_t out_n = size_t(std::max(0, orow1 - orow0)) * g.N;
+    if ((rc = ensure_buffer(&d->d_frame, &d->frame_cap, in_n))) return fail(rc);
+    if ((rc = ensure_buffer(&d->d_out, &d->out_cap, out_n))) return fail(rc);
+    if (!is_pinned(frame) && (rc = ensure_pinned(&d->h_in, &d->h_in_cap, in_n))) return fail(rc);
+    if (!is_pinned(out_band) && (rc = ensure_pinned(&d->h_out, &d->h_out_cap, out_n)))
+        return fail(rc);
+    // pinned caller buffers are copied directly; pageable ones go through staging
+    const bool in_pinned = is_pinned(frame), out_pinned = is_pinned(out_band);
+    const double* src = frame + size_t(fr0) * frame_cols;
+    if (!in_pinned) {
+        std::memcpy(d->h_in, src, sizeof(double) * in_n);
+        src = d->h_in;
+    }
+    cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
+    SolveArgs a = base_args(p, d);
+    a.frame = d->d_frame;
+    a.frame_rows = frame_rows;
+    a.frame_cols = frame_cols;
+    a.frame_row0 = fr0;
+    a.frame_pitch = frame_cols;
+    a.out = d->d_out;
+    a.out_row0 = orow0;
+    a.out_rows = g.M;
+    a.out_cols = g.N;
+    a.tasks = w->d_tasks;
+    a.items = w->d_items;
+    a.n_items = w->n_items;
+    cudaEventRecord(d->ev0, d->stream);
+    if (w->n_items > 0) {
+        if ((rc = launch(p, d, a, d->stream))) return fail(rc);
+        r->launches += 1;
+    }
+    cudaEventRecord(d->ev1, d->stream);
+    cudaMemcpyAsync(out_pinned ? out_band : d->h_out, d->d_out, sizeof(double) * out_n,
+                    cudaMemcpyDeviceToHost, d->stream);
+    cudaError_t e = cudaStreamSynchronize(d->stream);
+    if (e != cudaSuccess)
+        return fail(set_error(TQSB_ECUDA, std::string("solve: ") + cudaGetErrorString(e)));
+    cudaEventElapsedTime(&r->ms, d->ev0, d->ev1);
+    if (!out_pinned) std::memcpy(out_band, d->h_out, sizeof(double) * out_n);
+}
+
+void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const Geometry& g,
+                 long long classes_total, long long classes_interior, double e2e) {
+    if (!rep) return;
+    std::memset(rep, 0, sizeof(*rep));
+    double sec = 0, warm = 0;
+    long long blocks = 0, created = 0;
+    int launches = 0;
+    for (const auto& r : rs) {
+        sec = std::max(sec, double(r.ms) * 1e-3);
+        warm = std::max(warm, r.warm);
+        blocks += r.blocks;
+        created = std::max<long long>(created, r.created);
+        launches += r.launches;
+    }
+    rep->seconds = sec;
+    rep->warm_seconds = warm;
+    rep->e2e_seconds = e2e;
+    rep->blocks_processed = blocks;
+    rep->classes_total = classes_total;
+    rep->classes_interior = classes_interior;
+    rep->classes_created = created;
+    // reference semantics: one lookup per class in the warm pass, one per block
+    rep->cache_misses = created;
+    rep->cache_hits = blocks + (classes_total - created);
+    rep->psnr_db = 0.0;
+    rep->has_psnr = 0;
+    rep->gpu_launches = launches;
+    (void)g;
+}
+
+double psnr_impl(const double* a, const double* b, long long n) {
+    double sum = 0.0;
+    for (long long i = 0; i < n; ++i) {
+        const double d = a[i] - b[i];
+        sum += d * d;
+    }
+    const double mse = sum / double(n);
+    if (mse == 0.0) return std::numeric_limits<double>::infinity();
+    return -10.0 * std::log10(mse);
+}
+
+} // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* tqsb_last_error(void) { return g_error.c_str(); }
+const char* tqsb_version(void) { return "tqsb 0.1 (sm_100a)"; }
+
+void tqsb_config_default(tqsb_config* c) {
+    c->window = 32;
+    c->block = 4;
+    c->max_iterations = 200;
+    c->step_width = 0.5;
+    c->spatial_decay = 0.8;
+    c->frequency_exponent = 2.0;
+    c->precision = TQSB_PRECISION_DOUBLE;
+    c->clip_output = 1;
+    c->threads = 1;
+    c->compute = TQSB_COMPUTE_FP32;
+    c->hot_columns = -1;
+}
+
+int tqsb_validate_config(const tqsb_config* cfg, int period) {
+    if (!cfg) return set_error(TQSB_EINVAL, "null config");
+    return validate(*cfg, period);
+}
+
+int tqsb_census(int frame_rows, int frame_cols, const tqsb_config* cfg, int period,
+                long long out[3]) {
+    if (!cfg || !out) return set_error(TQSB_EINVAL, "null argument");
+    TQSB_TRY(validate(*cfg, period));
+    Geometry g;
+    TQSB_TRY(geometry(*cfg, frame_rows, frame_cols, &g));
+    Enumerated e;
+    enumerate(g, period, 0, g.padM / g.B, &e);
+    out[0] = (long long)e.tasks.size();
+    out[1] = e.classes_total;
+    out[2] = e.classes_interior;
+    return TQSB_OK;
+}
+
+int tqsb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int tqsb_plan_create(const uint8_t* opaque, int period, const tqsb_config* cfg,
+                     const int* devices, int n_devices, tqsb_plan** out) {
+    if (!out || !cfg || !opaque) return set_error(TQSB_EINVAL, "null argument");
+    *out = nullptr;
+    if (period < 4 || period % 2 != 0)
+        return set_error(TQSB_EINVAL, "pattern period must be even and >= 4");
+    TQSB_TRY(validate(*cfg, period));
+    TQSB_TRY(validate_device_limits(*cfg));
+    if (n_devices < 1) return set_error(TQSB_EINVAL, "at least one device is required");
+    const int have = tqsb_device_count();
+    if (have < 1) return set_error(TQSB_ENODEV, "no CUDA device available (no CPU fallback)");
+    auto p = std::make_unique<tqsb_plan>();
+    p->cfg = *cfg;
+    p->period = period;
+    p->opaque.assign(opaque, opaque + size_t(period / 2) * (period / 2));
+    for (uint8_t q : p->opaque)
+        if (q > 3) return set_error(TQSB_EINVAL, "quadrant indices must be in 0..3");
+    p->wt = window_tables(*cfg);
+    for (int i = 0; i < n_devices; ++i) {
+        const int id = devices ? devices[i] : i;
+        if (id < 0 || id >= have) return set_error(TQSB_ENODEV, "device index out of range");
+        auto d = std::make_unique<Device>();
+        d->id = id;
+        int rc = device_init(p.get(), d.get());
+        p->devs.push_back(std::move(d));
+        if (rc) {
+            for (auto& dd : p->devs) device_free(dd.get());
+            return rc;
+        }
+    }
+    *out = p.release();
+    return TQSB_OK;
+}
+
+int tqsb_plan_destroy(tqsb_plan* p) {
+    if (!p) return TQSB_OK;
+    for (auto& d : p->devs) device_free(d.get());
+    delete p;
+    return TQSB_OK;
+}
+
+int tqsb_plan_stats(const tqsb_plan* p, long long* classes, long long* bytes) {
+    if (!p) return set_error(TQSB_EINVAL, "null plan");
+    if (classes) *classes = p->devs.empty() ? 0 : (long long)p->devs[0]->tabs.size();
+    if (bytes) *bytes = p->devs.empty() ? 0 : (long long)p->devs[0]->table_bytes;
+    return TQSB_OK;
+}
+
+int tqsb_plan_warm(tqsb_plan* p, int frame_rows, int frame_cols, double* warm_seconds) {
+    if (!p) return set_error(TQSB_EINVAL, "null plan");
+    std::lock_guard<std::mutex> lk(p->mu);
+    Geometry g;
+    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    const auto t0 = std::chrono::steady_clock::now();
+    Enumerated e;
+    enumerate(g, p->period, 0, g.padM / g.B, &e);
+    for (auto& d : p->devs) {
+        int created = 0, launches = 0;
+        TQSB_TRY(ensure_classes(p, d.get(), e.class_order, e.representative, &created, &launches));
+    }
+    for (auto& d : p->devs) {
+        cudaSetDevice(d->id);
+        CUDA_TRY(cudaStreamSynchronize(d->stream));
+    }
+    if (warm_seconds)
+        *warm_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return TQSB_OK;
+}
+
+int tqsb_reconstruct_band(tqsb_plan* p, const double* frame, int frame_rows, int frame_cols,
+                          int br0, int br1, double* out_band, tqsb_report* rep) {
+    if (!p || !frame || !out_band) return set_error(TQSB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    const auto t0 = std::chrono::steady_clock::now();
+    Geometry g;
+    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    if (br0 < 0 || br1 > g.padM / g.B || br0 > br1)
+        return set_error(TQSB_EINVAL, "block-row band out of range");
+    std::vector<BandResult> rs(1);
+    run_band_host(p, p->devs[0].get(), g, frame, frame_rows, frame_cols, br0, br1, out_band, &rs[0]);
+    if (rs[0].rc) return set_error(rs[0].rc, rs[0].err);
+    fill_report(rep, rs, g, rs[0].classes_total, rs[0].classes_interior,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    return TQSB_OK;
+}
+
+int tqsb_reconstruct(tqsb_plan* p, const double* frame, int frame_rows, int frame_cols,
+                     double* out, const double* reference, tqsb_report* rep) {
+    if (!p || !frame || !out) return set_error(TQSB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    const auto t0 = std::chrono::steady_clock::now();
+    Geometry g;
+    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    const int nbr = g.padM / g.B;
+    const int nd = std::min<int>(int(p->devs.size()), std::max(1, nbr));
+    std::vector<BandResult> rs(nd);
+    std::vector<int> cut(nd + 1);
+    for (int i = 0; i <= nd; ++i) cut[i] = int((long long)nbr * i / nd);
+    if (nd == 1) {
+        run_band_host(p, p->devs[0].get(), g, frame, frame_rows, frame_cols, 0, nbr, out, &rs[0]);
+    } else {
+        std::vector<std::thread> th;
+        for (int i = 0; i < nd; ++i)
+            th.emplace_back([&, i] {
+                double* ob = out + size_t(cut[i]) * g.B * g.N;
+                run_band_host(p, p->devs[i].get(), g, frame, frame_rows, frame_cols, cut[i],
+                              cut[i + 1], ob, &rs[i]);
+            });
+        for (auto& t : th) t.join();
+    }
+    for (auto& r : rs)
+        if (r.rc) return set_error(r.rc, r.err);
+    // census of the whole frame (bands may share classes)
+    Enumerated e;
+    long long ct = rs[0].classes_total, ci = rs[0].classes_interior;
+    if (nd > 1) {
+        enumerate(g, p->period, 0, nbr, &e);
+        ct = e.classes_total;
+        ci = e.classes_interior;
+    }
+    const double e2e = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    fill_report(rep, rs, g, ct, ci, e2e);
+    if (reference) {
+        const double v = psnr_impl(reference, out, (long long)g.M * g.N);
+        if (rep) {
+            rep->psnr_db = v;
+            rep->has_psnr = 1;
+        }
+    }
+    return TQSB_OK;
+}
+
+static int device_band(tqsb_plan* p, const double* d_frame, int frame_rows, int frame_cols,
+                       int br0, int br1, double* d_out, void* stream, tqsb_report* rep) {
+    std::lock_guard<std::mutex> lk(p->mu);
+    Geometry g;
+    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    if (br0 < 0 || br1 > g.padM / g.B || br0 > br1)
+        return set_error(TQSB_EINVAL, "block-row band out of range");
+    Device* d = p->devs[0].get();
+    CUDA_TRY(cudaSetDevice(d->id));
+    Work* w = nullptr;
+    int created = 0, launches = 0;
+    TQSB_TRY(prepare_band(p, d, g, frame_rows, frame_cols, br0, br1, &w, &created, &launches));
+    SolveArgs a = base_args(p, d);
+    a.frame = d_frame;
+    a.frame_rows = frame_rows;
+    a.frame_cols = frame_cols;
+    a.frame_row0 = 0;
+    a.frame_pitch = frame_cols;
+    a.out = d_out;
+    a.out_row0 = br0 * g.B;
+    a.out_rows = g.M;
+    a.out_cols = g.N;
+    a.tasks = w->d_tasks;
+    a.items = w->d_items;
+    a.n_items = w->n_items;
+    if (w->n_items > 0) {
+        TQSB_TRY(launch(p, d, a, static_cast<cudaStream_t>(stream)));
+        launches += 1;
+    }
+    if (rep) {
+        std::memset(rep, 0, sizeof(*rep));
+        rep->blocks_processed = w->n_tasks;
+        rep->classes_total = w->classes_total;
+        rep->classes_interior = w->classes_interior;
+        rep->classes_created = created;
+        rep->cache_misses = created;
+        rep->cache_hits = w->n_tasks + (w->classes_total - created);
+        rep->gpu_launches = launches;
+    }
+    return TQSB_OK;
+}
+
+int tqsb_reconstruct_device(tqsb_plan* p, const double* d_frame, int frame_rows, int frame_cols,
+                            double* d_out, void* stream, tqsb_report* rep) {
+    if (!p || !d_frame || !d_out) return set_error(TQSB_EINVAL, "null argument");
+    Geometry g;
+    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    return device_band(p, d_frame, frame_rows, frame_cols, 0, g.padM / g.B, d_out, stream, rep);
+}
+
+int tqsb_reconstruct_band_device(tqsb_plan* p, const double* d_frame, int frame_rows,
+                                 int frame_cols, int br0, int br1, double* d_out, void* stream,
+                                 tqsb_report* rep) {
+    if (!p || !d_frame || !d_out) return set_error(TQSB_EINVAL, "null argument");
+    return device_band(p, d_frame, frame_rows, frame_cols, br0, br1, d_out, stream, rep);
+}
+
+int tqsb_plan_export_tables(tqsb_plan* p, int orow, int ocol, int* local_out, double* b_re,
+                            double* b_im, double* c_re, double* c_im, double* dd) {
+    if (!p || !local_out) return set_error(TQSB_EINVAL, "null argument");
+    if (orow < 0 || ocol < 0) return set_error(TQSB_EINVAL, "window origin must be non-negative");
+    std::lock_guard<std::mutex> lk(p->mu);
+    Device* d = p->devs[0].get();
+    const int key = (orow % p->period) * p->period + (ocol % p->period);
+    std::map<int, std::pair<int, int>> rep{{key, {orow, ocol}}};
+    int created = 0, launches = 0;
+    TQSB_TRY(ensure_classes(p, d, {key}, rep, &created, &launches));
+    const ClassTab& t = d->tabs[d->slot_of.at(key)];
+    *local_out = t.local;
+    if (!b_re) return TQSB_OK;
+    const size_t K = p->wt.K, L = t.local;
+    std::vector<double> b(K * L * 2), c(K * K * 2);
+    CUDA_TRY(cudaSetDevice(d->id));
+    CUDA_TRY(cudaMemcpy(b.data(), t.b64, sizeof(double) * b.size(), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(c.data(), t.c64, sizeof(double) * c.size(), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(dd, t.d64, sizeof(double) * K, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < K * L; ++i) {
+        b_re[i] = b[2 * i];
+        b_im[i] = b[2 * i + 1];
+    }
+    for (size_t i = 0; i < K * K; ++i) {
+        c_re[i] = c[2 * i];
+        c_im[i] = c[2 * i + 1];
+    }
+    return TQSB_OK;
+}
+
+int tqsb_plan_block_trace(tqsb_plan* p, int orow, int ocol, const double* y_local, int* picks,
+                          double* gd, double* window_out, int* n_out) {
+    if (!p || !y_local || !picks || !gd || !n_out) return set_error(TQSB_EINVAL, "null argument");
+    if (orow < 0 || ocol < 0) return set_error(TQSB_EINVAL, "window origin must be non-negative");
+    std::lock_guard<std::mutex> lk(p->mu);
+    Device* d = p->devs[0].get();
+    const int W = p->cfg.window, B = p->cfg.block;
+    const int key = (orow % p->period) * p->period + (ocol % p->period);
+    std::map<int, std::pair<int, int>> rep{{key, {orow, ocol}}};
+    int created = 0, launches = 0;
+    TQSB_TRY(ensure_classes(p, d, {key}, rep, &created, &launches));
+    // a frame holding y_local at the window's cells (gather_local_values order)
+    const int r0 = (orow + 1) / 2, r1 = (orow + W - 2) / 2;
+    const int c0 = (ocol + 1) / 2, c1 = (ocol + W - 2) / 2;
+    const int fr = (orow + W) / 2 + 1, fc = (ocol + W) / 2 + 1;
+    std::vector<double> frame(size_t(fr) * fc, 0.0);
+    int m = 0;
+    for (int r = r0; r <= r1; ++r)
+        for (int c = c0; c <= c1; ++c) frame[size_t(r) * fc + c] = y_local[m++];
+    const int lead = (W - B) / 2;
+    Task t{orow + lead, ocol + lead, orow, ocol};
+    WorkItem wi{d->slot_of.at(key), 0, 1, 0};
+    const int iters = std::max(1, p->cfg.max_iterations);
+    CUDA_TRY(cudaSetDevice(d->id));
+    char* buf = nullptr;
+    const size_t out_n = size_t(B) * (t.block_col + B);
+    const size_t bytes = sizeof(double) * frame.size() + sizeof(double) * out_n + sizeof(Task) +
+                         sizeof(WorkItem) + sizeof(int) * iters + sizeof(double) * 2 * iters +
+                         sizeof(double) * W * W + sizeof(int) + 1024;
+    CUDA_TRY(cudaMalloc(&buf, bytes));
+    size_t off = 0;
+    auto take = [&](size_t n) {
+        char* q = buf + off;
+        off = align_up(off + n, 64);
+        return q;
+    };
+    double* d_frame = reinterpret_cast<double*>(take(sizeof(double) * frame.size()));
+    double* d_out = reinterpret_cast<double*>(take(sizeof(double) * out_n));
+    Task* d_task = reinterpret_cast<Task*>(take(sizeof(Task)));
+    WorkItem* d_item = reinterpret_cast<WorkItem*>(take(sizeof(WorkItem)));
+    int* d_picks = reinterpret_cast<int*>(take(sizeof(int) * iters));
+    double* d_gd = reinterpret_cast<double*>(take(sizeof(double) * 2 * iters));
+    double* d_win = reinterpret_cast<double*>(take(sizeof(double) * W * W));
+    int* d_n = reinterpret_cast<int*>(take(sizeof(int)));
+    cudaMemcpy(d_frame, frame.data(), sizeof(double) * frame.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(d_task, &t, sizeof(Task), cudaMemcpyHostToDevice);
+    cudaMemcpy(d_item, &wi, sizeof(WorkItem), cudaMemcpyHostToDevice);
+    cudaMemset(d_n, 0, sizeof(int));
+    SolveArgs a = base_args(p, d);
+    a.frame = d_frame;
+    a.frame_rows = fr;
+    a.frame_cols = fc;
+    a.frame_row0 = 0;
+    a.frame_pitch = fc;
+    a.out = d_out;
+    a.out_row0 = t.block_row;
+    a.out_rows = t.block_row + B;
+    a.out_cols = t.block_col + B;
+    a.tasks = d_task;
+    a.items = d_item;
+    a.n_items = 1;
+    a.trace_picks = d_picks;
+    a.trace_gd = d_gd;
+    a.trace_window = window_out ? d_win : nullptr;
+    a.trace_n = d_n;
+    int rc = launch(p, d, a, d->stream);
+    if (rc) {
+        cudaFree(buf);
+        return rc;
+    }
+    cudaError_t e = cudaStreamSynchronize(d->stream);
+    if (e != cudaSuccess) {
+        cudaFree(buf);
+        return set_error(TQSB_ECUDA, std::string("trace: ") + cudaGetErrorString(e));
+    }
+    int n = 0;
+    cudaMemcpy(&n, d_n, sizeof(int), cudaMemcpyDeviceToHost);
+    *n_out = n;
+    cudaMemcpy(picks, d_picks, sizeof(int) * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(gd, d_gd, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost);
+    if (window_out) cudaMemcpy(window_out, d_win, sizeof(double) * W * W, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    return TQSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host helpers: input side and test support
+// ---------------------------------------------------------------------------
+int tqsb_generate_pattern(uint64_t seed, int period, int block, uint8_t* opaque_out) {
+    if (!opaque_out) return set_error(TQSB_EINVAL, "null argument");
+    if (period < 4 || period % 2 != 0)
+        return set_error(TQSB_EINVAL, "pattern period must be even and >= 4");
+    if (block < 1 || period % block != 0)
+        return set_error(TQSB_EINVAL, "pattern period must be divisible by the target block size");
+    std::mt19937_64 gen(seed);
+    const size_t n = size_t(period / 2) * (period / 2);
+    for (size_t i = 0; i < n; ++i) opaque_out[i] = static_cast<uint8_t>(gen() & 3u);
+    return TQSB_OK;
+}
+
+int tqsb_simulate(const double* image, int rows, int cols, const uint8_t* opaque, int period,
+                  double* frame_out) {
+    if (!image || !opaque || !frame_out) return set_error(TQSB_EINVAL, "null argument");
+    if (rows % 2 != 0 || cols % 2 != 0) return set_error(TQSB_EINVAL, "image dimensions must be even");
+    if (period <= 0) return set_error(TQSB_EINVAL, "invalid pattern");
+    const int pc = period / 2, fr = rows / 2, fc = cols / 2;
+    const double third = 1.0 / 3.0;
+    for (int r = 0; r < fr; ++r)
+        for (int c = 0; c < fc; ++c) {
+            const int q = opaque[size_t(r % pc) * pc + c % pc];
+            double acc = 0.0;
+            for (int quad = 0; quad < 4; ++quad)
+                if (quad != q)
+                    acc += third * image[size_t(2 * r + quad / 2) * cols + 2 * c + quad % 2];
+            frame_out[size_t(r) * fc + c] = acc;
+        }
+    return TQSB_OK;
+}
+
+// Smooth synthetic test scene: linear ramp + 6 plane waves + 5 Gaussian bumps +
+// 2 logistic edges, rescaled to [0.02, 0.98]; parameters drawn in that order from
+// mt19937_64(seed) through uniform_real_distribution(0,1)
+// (the generator of tests/support/synthetic.cpp:9-80).
+int tqsb_synthetic_image(int rows, int cols, uint64_t seed, double* out) {
+    if (!out || rows < 1 || cols < 1) return set_error(TQSB_EINVAL, "invalid image shape");
+    std::mt19937_64 gen(seed);
+    std::uniform_real_distribution<double> U(0.0, 1.0);
+    const double two_pi = 6.283185307179586;
+    const double ramp_r = U(gen) * 2.0 - 1.0;
+    const double ramp_c = U(gen) * 2.0 - 1.0;
+    double wave[6][4];
+    for (auto& wv : wave) {
+        wv[0] = (U(gen) * 6.0 + 0.5) / rows;
+        wv[1] = (U(gen) * 6.0 + 0.5) / cols;
+        wv[2] = U(gen) * two_pi;
+        wv[3] = U(gen) * 0.5 + 0.1;
+    }
+    double bump[5][4];
+    const double short_side = std::min(rows, cols);
+    for (auto& bp : bump) {
+        bp[0] = U(gen) * rows;
+        bp[1] = U(gen) * cols;
+        bp[2] = (U(gen) * 0.12 + 0.04) * short_side;
+        bp[3] = (U(gen) * 2.0 - 1.0) * 0.8;
+    }
+    double edge[2][4];
+    for (auto& ed : edge) {
+        const double theta = U(gen) * two_pi;
+        ed[0] = std::sin(theta);
+        ed[1] = std::cos(theta);
+        ed[2] = U(gen) * (rows + cols) * 0.5;
+        ed[3] = (U(gen) * 2.0 - 1.0) * 0.6;
+    }
+    double vmin = 1e300, vmax = -1e300;
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+            double v = ramp_r * r / rows + ramp_c * c / cols;
+            for (const auto& wv : wave) v += wv[3] * std::sin(two_pi * (wv[0] * r + wv[1] * c) + wv[2]);
+            for (const auto& bp : bump) {
+                const double dy = r - bp[0], dx = c - bp[1];
+                v += bp[3] * std::exp(-(dy * dy + dx * dx) / (2.0 * bp[2] * bp[2]));
+            }
+            for (const auto& ed : edge)
+                v += ed[3] / (1.0 + std::exp(-(ed[0] * r + ed[1] * c - ed[2]) / 2.5));
+            out[size_t(r) * cols + c] = v;
+            vmin = std::min(vmin, v);
+            vmax = std::max(vmax, v);
+        }
+    const double span = vmax > vmin ? vmax - vmin : 1.0;
+    for (size_t i = 0; i < size_t(rows) * cols; ++i) out[i] = 0.02 + 0.96 * (out[i] - vmin) / span;
+    return TQSB_OK;
+}
+
+double tqsb_psnr(const double* reference, const double* estimate, long long n) {
+    if (!reference || !estimate || n <= 0) return std::numeric_limits<double>::quiet_NaN();
+    return psnr_impl(reference, estimate, n);
+}
+
+void* tqsb_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+        set_error(TQSB_ENOMEM, "cudaHostAlloc failed");
+        return nullptr;
+    }
+    return p;
+}
+
+void tqsb_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+int tqsb_probe_peaks(int device, double* fp32_tflops, double* smem_tbps) {
+    if (tqsb_device_count() < 1) return set_error(TQSB_ENODEV, "no CUDA device available");
+    const int rc = probe_peaks(device, fp32_tflops, smem_tbps);
+    if (rc) return set_error(TQSB_ECUDA, cudaGetErrorString(cudaError_t(rc)));
+    return TQSB_OK;
+}
+
+} // extern "C"

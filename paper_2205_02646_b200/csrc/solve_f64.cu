@@ -1,0 +1,177 @@
+// solve_f64.cu -- the fp64 PARITY mode of the block solve (TQSB_COMPUTE_FP64).
+//
+// The reference's block_impl (rljsde.cpp:122-182) restated per warp on device
+// in double precision on the reference-ordered tables (B k-major, C column-major,
+// D; tables.cu): init R = B y in m order (127-138), selection q|R|^2/D with the
+// strict '>' first-max rule (144-158, basis.hpp:90-92), the coefficient step and
+// column cascade (160-172), then synthesize_real (basis.cpp:52-73) restricted to
+// the kept B x B pixels over the active list in first-touch order, placement
+// with optional clip (pipeline.cpp:157-166). Its purpose is to prove that the
+// device pipeline (enumeration, classes, tables, gather, placement) reproduces
+// the reference's greedy paths; the fp32 kernel (solve_f32.cu) is the product.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tqsb_internal.hpp"
+
+namespace tqsb {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a) {
+    extern __shared__ __align__(16) double sm64[];
+    const int W = a.window, K = W * W, B = a.block;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // per warp: R (2K), coef (2K), y (K/4+..: use K), order (K ints), touched (K bytes)
+    const size_t per = size_t(5) * K + K / 2 + K / 8 + 8;
+    double* base = sm64 + warp * per;
+    double* Rr = base;
+    double* Ri = Rr + K;
+    double* cr = Ri + K;
+    double* ci = cr + K;
+    double* y = ci + K;
+    int* order = reinterpret_cast<int*>(y + K);
+    unsigned char* touched = reinterpret_cast<unsigned char*>(order + K);
+
+    const int gw = blockIdx.x * kWarpsF64 + warp, nw = gridDim.x * kWarpsF64;
+    for (int it_item = 0; it_item < a.n_items; ++it_item) {
+        const WorkItem item = a.items[it_item];
+        const ClassTab& ct = a.tabs[item.cls];
+        const int L = ct.local;
+        for (int ti = item.start + gw; ti < item.start + item.count; ti += nw) {
+            const Task tk = a.tasks[ti];
+            // gather_local_values (grid.cpp:104-114); pad_frame by clamping (pipeline.cpp:44-52)
+            const int r0 = (tk.origin_row + 1) / 2, r1 = (tk.origin_row + W - 2) / 2;
+            const int c0 = (tk.origin_col + 1) / 2, c1 = (tk.origin_col + W - 2) / 2;
+            const int ncol = c1 - c0 + 1;
+            for (int m = lane; m < L; m += 32) {
+                int fr = r0 + m / ncol, fc = c0 + m % ncol;
+                fr = fr < a.frame_rows - 1 ? fr : a.frame_rows - 1;
+                fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
+                y[m] = a.frame[size_t(fr - a.frame_row0) * a.frame_pitch + fc];
+                (void)r1;
+            }
+            for (int k = lane; k < K; k += 32) {
+                cr[k] = 0.0;
+                ci[k] = 0.0;
+                touched[k] = 0;
+            }
+            __syncwarp();
+            for (int k = lane; k < K; k += 32) {  // R = B y  (rljsde.cpp:127-138)
+                const double* col = ct.b64 + size_t(k) * L * 2;
+                double re = 0.0, im = 0.0;
+                for (int m = 0; m < L; ++m) {
+                    re += col[2 * m] * y[m];
+                    im += col[2 * m + 1] * y[m];
+                }
+                Rr[k] = re;
+                Ri[k] = im;
+            }
+            __syncwarp();
+            const bool tracing = a.trace_picks != nullptr && ti == 0;
+            int nactive = 0, it = 0;
+            for (; it < a.iterations; ++it) {
+                int best = -1;
+                double bs = 0.0;
+                for (int k = lane; k < K; k += 32) {
+                    const double dk = ct.d64[k];
+                    if (dk <= 0.0) continue;
+                    const double s = a.wc.q64[k] * (Rr[k] * Rr[k] + Ri[k] * Ri[k]) / dk;
+                    if (best < 0 || s > bs) {
+                        best = k;
+                        bs = s;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double os = __shfl_xor_sync(FULL, bs, off);
+                    const int ok = __shfl_xor_sync(FULL, best, off);
+                    const bool take = ok >= 0 && (best < 0 || os > bs || (os == bs && ok < best));
+                    if (take) {
+                        bs = os;
+                        best = ok;
+                    }
+                }
+                if (best < 0) break;
+                const int u = best;
+                const double du = ct.d64[u];
+                const double gr = a.step * (Rr[u] / du), gi = a.step * (Ri[u] / du);
+                __syncwarp();
+                const bool fresh = touched[u] == 0;
+                __syncwarp();
+                if (lane == 0) {
+                    cr[u] += gr;
+                    ci[u] += gi;
+                    if (fresh) {
+                        touched[u] = 1;
+                        order[nactive] = u;
+                    }
+                    if (tracing) {
+                        a.trace_picks[it] = u;
+                        a.trace_gd[2 * it] = gr;
+                        a.trace_gd[2 * it + 1] = gi;
+                    }
+                }
+                if (fresh) ++nactive;
+                const double* col = ct.c64 + size_t(u) * K * 2;
+                for (int s = lane; s < K; s += 32) {
+                    const double c_r = col[2 * s], c_i = col[2 * s + 1];
+                    Rr[s] -= gr * c_r - gi * c_i;
+                    Ri[s] -= gr * c_i + gi * c_r;
+                }
+                __syncwarp();
+            }
+            __syncwarp();
+            // synthesize_real over the kept pixels (basis.cpp:52-73), then place
+            const int rw = tk.block_row - tk.origin_row, cw = tk.block_col - tk.origin_col;
+            for (int p = lane; p < B * B; p += 32) {
+                const int eta = rw + p / B, gam = cw + p % B;
+                double v = 0.0;
+                for (int t = 0; t < nactive; ++t) {
+                    const int f = order[t];
+                    const int idx = (eta * (f / W) + gam * (f % W)) % W;
+                    v += cr[f] * a.wc.unit64[2 * idx] - ci[f] * a.wc.unit64[2 * idx + 1];
+                }
+                const int orow = tk.block_row + p / B, ocol = tk.block_col + p % B;
+                if (orow < a.out_rows && ocol < a.out_cols) {
+                    if (a.clip) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+                    a.out[size_t(orow - a.out_row0) * a.out_cols + ocol] = v;
+                }
+            }
+            if (tracing) {
+                if (lane == 0) *a.trace_n = it;
+                if (a.trace_window) {
+                    for (int p = lane; p < K; p += 32) {
+                        const int eta = p / W, gam = p % W;
+                        double v = 0.0;
+                        for (int t = 0; t < nactive; ++t) {
+                            const int f = order[t];
+                            const int idx = (eta * (f / W) + gam * (f % W)) % W;
+                            v += cr[f] * a.wc.unit64[2 * idx] - ci[f] * a.wc.unit64[2 * idx + 1];
+                        }
+                        a.trace_window[p] = v;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+} // namespace
+
+int launch_solve_f64(const SolveArgs& a, void* stream, int num_sms) {
+    const int K = a.window * a.window;
+    const size_t per = size_t(5) * K + K / 2 + K / 8 + 8;
+    const size_t smem = per * sizeof(double) * kWarpsF64;
+    cudaError_t e = cudaFuncSetAttribute(k_solve_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    int grid = num_sms * 2;
+    k_solve_f64<<<grid, kWarpsF64 * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    return cudaGetLastError();
+}
+
+} // namespace tqsb

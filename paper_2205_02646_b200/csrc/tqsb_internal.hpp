@@ -1,0 +1,108 @@
+// tqsb_internal.hpp -- shared between the host orchestration (plan.cpp) and the
+// CUDA translation units (tables.cu, solve_f32.cu, solve_f64.cu). No CUDA types
+// here so plan.cpp compiles with plain g++.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace tqsb {
+
+constexpr int kMaxWindow = 32;  // device paths hold a warp-row per window row/col
+constexpr int kWarpsF32 = 12;   // warps per CTA of the fp32 solve kernel (1 CTA/SM, <=168 regs)
+constexpr int kWarpsF64 = 4;    // warps per CTA of the fp64 parity kernel
+constexpr int kSbufStride = 20; // floats per lane in the slot-max buffer (conflict-free STS.128)
+
+// One target block: top-left output pixel and clamped window origin
+// (BlockTask, pipeline.cpp:54-58), plus its class slot in the plan.
+struct Task {
+    int block_row, block_col, origin_row, origin_col;
+};
+
+// A run of consecutive class-sorted tasks handled by one CTA pass.
+struct WorkItem {
+    int cls;    // class slot (index into the ClassTab array)
+    int start;  // first task
+    int count;  // number of tasks
+    int pad;
+};
+
+// Device-resident tables of one offset class (the KernelSet analogue,
+// rljsde.hpp:34-52), all pointers into device memory of one GPU.
+struct ClassTab {
+    // fp32 product tables (rank order)
+    const float* cpack;   // K_pad columns x (K_pad/2) float4: C'[s,u] = s_s * C[s,u]
+    const float* scale;   // K_pad: s_r = sqrt(q/D) (NaN where D <= 0 or padding)
+    const float* fac;     // K_pad: gamma / (s_u * D_u)
+    const float* mask32;  // W*W: w_m/3 at transparent pixels of included cells, else 0
+    // fp64 parity tables (reference order)
+    const double* b64;    // K*L complex interleaved, k-major [k*L+m]
+    const double* c64;    // K*K complex interleaved, column-major [uk*K+sk]
+    const double* d64;    // K
+    const int* cells;     // L x (cell frame row offset, cell frame col offset) vs window origin
+    int local;            // L
+    int pad;
+};
+
+// Per-window constants (class independent), device pointers.
+struct WindowConsts {
+    const int* perm;       // K_pad: rank -> flat k (or -1 for padding ranks)
+    const int* src;        // K_pad: rank -> half-spectrum buffer index, bit 30 = conjugate
+    const float* unit32;   // 2*W: (cos, sin) of 2*pi*k/W, the FourierTable (basis.cpp:15-26)
+    const double* unit64;  // 2*W
+    const double* q64;     // K: frequency_weights (basis.cpp:99-106)
+};
+
+struct SolveArgs {
+    const double* frame;   // device frame (full frame, or a row band starting at frame_row0)
+    int frame_rows;        // rows of the UNPADDED full frame (clamping implements pad_frame)
+    int frame_cols;
+    int frame_row0;        // first frame row held at frame[0]
+    int frame_pitch;       // elements per frame row in the buffer
+    double* out;           // output rows starting at out_row0
+    int out_row0;
+    int out_rows;          // rows of the unpadded output image (M); crop beyond
+    int out_cols;          // N (also the pitch)
+    const Task* tasks;
+    const WorkItem* items;
+    int n_items;
+    const ClassTab* tabs;
+    WindowConsts wc;
+    int window, block, iterations;
+    double step;
+    int clip;
+    int hot;               // columns cached in shared memory (fp32)
+    // tracing (single-block diagnostics): when trace_picks != nullptr, block 0
+    // records picks (flat k), gd (re,im) and the full window synthesis.
+    int* trace_picks;
+    double* trace_gd;
+    double* trace_window;
+    int* trace_n;
+};
+
+// ---- launchers (defined in the .cu files); return cudaError_t as int ----
+int launch_solve_f32(const SolveArgs& a, int n_slots, void* stream, int num_sms);
+int launch_solve_f64(const SolveArgs& a, void* stream, int num_sms);
+size_t solve_f32_smem_bytes(int n_slots, int hot);
+int solve_f32_max_hot(int n_slots, int device);
+
+// Per-class build descriptor for the batched table kernels (tables.cu).
+struct ClassBuild {
+    int local;                 // L
+    const signed char* px;     // L*6: (eta, gamma) of the 3 transparent pixels per cell
+    const double* w;           // L spatial weights (host-computed, basis.cpp:75-88)
+    double* t64;               // K*L*2 (re, im interleaved), k-major
+    double* b64;               // K*L*2
+    double* c64;               // K*K*2, column-major [uk*K+sk]
+    double* d64;               // K
+    float* cpack;              // K_pad * K_pad/2 * 4 (null: fp64-only plan)
+    float* scale;              // K_pad
+    float* fac;                // K_pad
+};
+int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, double step,
+                        const double* unit64, const double* q64, const int* perm,
+                        int max_local, void* stream, int* launches);
+
+int probe_peaks(int device, double* fp32_tflops, double* smem_tbps);
+
+} // namespace tqsb
