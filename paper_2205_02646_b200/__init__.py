@@ -25,7 +25,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtqsb.so")
+# TQSB_LIB selects an experiment variant built by build.py (default: the product library)
+LIB_PATH = os.environ.get("TQSB_LIB") or os.path.join(HERE, "libtqsb.so")
 
 TQSB_OK, TQSB_EINVAL, TQSB_ECUDA, TQSB_ENOMEM, TQSB_ELOGIC, TQSB_ENODEV = range(6)
 

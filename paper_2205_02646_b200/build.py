@@ -40,38 +40,49 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError("build failed: " + " ".join(cmd))
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, defines: list[str] | None = None, lib: str | None = None,
+          tag: str = "") -> str:
+    """defines/lib/tag: experiment variants (e.g. -DTQSB_WARPS_F32=8 into libtqsb_w8.so)."""
+    defines = [f"-D{d}" for d in (defines or [])]
+    build_dir = BUILD + tag
+    lib = lib or LIB
+    os.makedirs(build_dir, exist_ok=True)
     jobs = []
     objs = []
     for f in CU:
         src = os.path.join(CSRC, f)
-        obj = os.path.join(BUILD, f + ".o")
+        obj = os.path.join(build_dir, f + ".o")
         objs.append(obj)
         if _newer(obj, [src] + HEADERS):
-            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            jobs.append([NVCC, *ARCH, *defines, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                          "-Xptxas", "-warn-spills", "-I", INCLUDE, "-c", src, "-o", obj])
     for f in CPP:
         src = os.path.join(CSRC, f)
-        obj = os.path.join(BUILD, f + ".o")
+        obj = os.path.join(build_dir, f + ".o")
         objs.append(obj)
         if _newer(obj, [src] + HEADERS):
             # x86-64-v3 + contraction: the input generators then round exactly like the
             # reference build (g++ -O3 -march=native contracts a*b+c into FMA)
             jobs.append(["g++", "-std=c++17", "-O3", "-march=x86-64-v3", "-ffp-contract=fast",
-                         "-fPIC", "-Wall", "-Wextra", "-pthread",
+                         "-fPIC", "-Wall", "-Wextra", "-pthread", *defines,
                          "-I", os.path.join(CUDA, "include"), "-I", INCLUDE, "-c", src, "-o", obj])
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         for cmd in jobs:
             if verbose:
                 print(" ".join(cmd))
         list(ex.map(_run, jobs))
-    if _newer(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *objs,
+    if _newer(lib, objs):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs,
               "-Xcompiler", "-pthread"])
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose=True))
+    # python build.py [VARIANT_TAG DEFINE ...]  e.g.  python build.py w8 TQSB_WARPS_F32=8
+    if len(sys.argv) > 1:
+        tag = sys.argv[1]
+        print(build(verbose=True, defines=sys.argv[2:], tag="_" + tag,
+                    lib=os.path.join(HERE, f"libtqsb_{tag}.so")))
+    else:
+        print(build(verbose=True))

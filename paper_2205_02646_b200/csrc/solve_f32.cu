@@ -34,7 +34,28 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef TQSB_PREFETCH
+#define TQSB_PREFETCH 16  // C' slots in flight ahead of the update (register budget)
+#endif
+
 __device__ __forceinline__ float qnan() { return __int_as_float(0x7fc00000); }
+
+// STS.64 straight from an FFMA2 register pair (inline PTX keeps ptxas from fusing
+// neighbouring stores into an STS.128 that needs register copies to pack)
+__device__ __forceinline__ void st_shared_f2(float* p, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(p))),
+                 "f"(v.x), "f"(v.y)
+                 : "memory");
+}
+
+// warp-wide max in one CREDUX (redux.sync .f32, sm_100a); NaN inputs are ignored,
+// so the result is NaN only when every lane holds NaN (no admissible frequency)
+__device__ __forceinline__ float warp_max_f32(float x) {
+    float m;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(m) : "f"(x));
+    return m;
+}
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float d;
@@ -42,96 +63,169 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     return d;
 }
 
+// (re, im) of element t (slot t>>1, half t&1) of this lane's residual; t is
+// warp-uniform, so the switch is a uniform branch, not a local-memory array.
 template <int NS>
-__device__ __forceinline__ float4 pick_slot(const float4 (&R)[NS], int i) {
-    float4 v = R[0];
-    switch (i) {
-#define TQSB_CASE(n) \
-    case n:          \
-        if (n < NS) v = R[n < NS ? n : 0]; \
+__device__ __forceinline__ float2 pick_elem(const float4 (&R)[NS], int t) {
+    float re = 0.f, im = 0.f;
+    switch (t) {
+#define TQSB_CASE(n)                                                            \
+    case n:                                                                     \
+        if ((n >> 1) < NS) {                                                    \
+            re = (n & 1) ? R[(n >> 1) < NS ? (n >> 1) : 0].y : R[(n >> 1) < NS ? (n >> 1) : 0].x; \
+            im = (n & 1) ? R[(n >> 1) < NS ? (n >> 1) : 0].w : R[(n >> 1) < NS ? (n >> 1) : 0].z; \
+        }                                                                       \
         break;
         TQSB_CASE(0) TQSB_CASE(1) TQSB_CASE(2) TQSB_CASE(3) TQSB_CASE(4) TQSB_CASE(5)
         TQSB_CASE(6) TQSB_CASE(7) TQSB_CASE(8) TQSB_CASE(9) TQSB_CASE(10) TQSB_CASE(11)
-        TQSB_CASE(12) TQSB_CASE(13) TQSB_CASE(14) TQSB_CASE(15)
+        TQSB_CASE(12) TQSB_CASE(13) TQSB_CASE(14) TQSB_CASE(15) TQSB_CASE(16) TQSB_CASE(17)
+        TQSB_CASE(18) TQSB_CASE(19) TQSB_CASE(20) TQSB_CASE(21) TQSB_CASE(22) TQSB_CASE(23)
+        TQSB_CASE(24) TQSB_CASE(25) TQSB_CASE(26) TQSB_CASE(27) TQSB_CASE(28) TQSB_CASE(29)
+        TQSB_CASE(30) TQSB_CASE(31)
 #undef TQSB_CASE
         default: break;
     }
-    return v;
+    return make_float2(re, im);
 }
 
-// Scores |R'|^2 of every slot: slot maxima to sbuf (STS.128 per 4 slots), lane max returned.
+// Scores |R'|^2 of every element go to this lane's row of the score buffer (one
+// STS.64 per slot, straight from the FFMA2 register pair) and into the lane maximum (FMNMX3;
+// NaN marks an inadmissible frequency and is ignored by max).
 template <int NS>
-__device__ __forceinline__ float score_pass(const float4 (&R)[NS], int lane, float* sbuf) {
-    float lmax = qnan();
+__device__ __forceinline__ float score_pass(const float4 (&R)[NS], float* srow) {
+    float m4[4] = {qnan(), qnan(), qnan(), qnan()};  // 4 short FMNMX3 chains
 #pragma unroll
-    for (int i0 = 0; i0 < NS; i0 += 4) {
-        float m[4] = {qnan(), qnan(), qnan(), qnan()};
-#pragma unroll
-        for (int j = 0; j < 4 && i0 + j < NS; ++j) {
-            const float2 re = make_float2(R[i0 + j].x, R[i0 + j].y);
-            const float2 im = make_float2(R[i0 + j].z, R[i0 + j].w);
-            float2 s = __fmul2_rn(re, re);
-            s = __ffma2_rn(im, im, s);
-            m[j] = fmaxf(s.x, s.y);
-        }
-        if constexpr (NS >= 4) {
-            *reinterpret_cast<float4*>(sbuf + lane * kSbufStride + i0) =
-                make_float4(m[0], m[1], m[2], m[3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < NS; ++j) sbuf[lane * kSbufStride + j] = m[j];
-        }
-        lmax = fmax3(lmax, fmax3(m[0], m[1], m[2]), m[3]);
+    for (int i = 0; i < NS; ++i) {
+        const float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
+        const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
+        m4[i & 3] = fmax3(m4[i & 3], sc.x, sc.y);
+        st_shared_f2(srow + 2 * i, sc);
     }
-    return lmax;
+    return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
 }
 
-// R' -= g C'[:,u] for every slot (2 FFMA2 per complex element), fused with the scores.
-template <int NS>
-__device__ __forceinline__ float update_pass(float4 (&R)[NS], const float4* __restrict__ col,
-                                             int lane, float gre, float gim, float* sbuf) {
+// R' -= g C'[:,u] for every slot (4 FFMA2 per rank pair) from the prefetched
+// column c[], fused with the next scores.
+// PF slots of the column were issued before the pick (c[0..PF-1]); the rest stream
+// in a sliding window PF slots ahead of the update.
+template <int NS, int PF>
+__device__ __forceinline__ float update_pass(float4 (&R)[NS], float4 (&c)[NS],
+                                             const float4* __restrict__ col, int lane, float gre,
+                                             float gim, float* srow) {
     const float2 ngre = make_float2(-gre, -gre);
     const float2 pgim = make_float2(gim, gim);
     const float2 ngim = make_float2(-gim, -gim);
-    float lmax = qnan();
+    float m4[4] = {qnan(), qnan(), qnan(), qnan()};  // 4 short FMNMX3 chains
 #pragma unroll
-    for (int i0 = 0; i0 < NS; i0 += 4) {
-        float m[4] = {qnan(), qnan(), qnan(), qnan()};
-#pragma unroll
-        for (int j = 0; j < 4 && i0 + j < NS; ++j) {
-            const int i = i0 + j;
-            const float4 c = col[i * 32 + lane];
-            const float2 cre = make_float2(c.x, c.y), cim = make_float2(c.z, c.w);
-            float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
-            re = __ffma2_rn(ngre, cre, re);
-            re = __ffma2_rn(pgim, cim, re);
-            im = __ffma2_rn(ngre, cim, im);
-            im = __ffma2_rn(ngim, cre, im);
-            R[i] = make_float4(re.x, re.y, im.x, im.y);
-            float2 s = __fmul2_rn(re, re);
-            s = __ffma2_rn(im, im, s);
-            m[j] = fmaxf(s.x, s.y);
-        }
-        if constexpr (NS >= 4) {
-            *reinterpret_cast<float4*>(sbuf + lane * kSbufStride + i0) =
-                make_float4(m[0], m[1], m[2], m[3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < NS; ++j) sbuf[lane * kSbufStride + j] = m[j];
-        }
-        lmax = fmax3(lmax, fmax3(m[0], m[1], m[2]), m[3]);
+    for (int i = 0; i < NS; ++i) {
+        if (i + PF < NS) c[i + PF] = col[(i + PF) * 32 + lane];
+        const float2 cre = make_float2(c[i].x, c[i].y), cim = make_float2(c[i].z, c[i].w);
+        float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
+        re = __ffma2_rn(ngre, cre, re);
+        re = __ffma2_rn(pgim, cim, re);
+        im = __ffma2_rn(ngre, cim, im);
+        im = __ffma2_rn(ngim, cre, im);
+        R[i] = make_float4(re.x, re.y, im.x, im.y);
+        const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
+        m4[i & 3] = fmax3(m4[i & 3], sc.x, sc.y);
+        st_shared_f2(srow + 2 * i, sc);
     }
-    return lmax;
+    return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
 }
 
-// per-warp scratch floats: init half-spectrum buffer (W/2+1 rows x 32 complex,
-// row stride 18 complex for the transpose) vs the slot-max buffer (32 x 20)
+// ---------------------------------------------------------------------------
+// Tensor memory as the hot-column tier. TMEM is 512 columns x 128 lanes x 32 bit
+// per SM and a warp reaches only its lane quadrant (lanes 32*(warp%4)..+31), so
+// each quadrant holds its own copy of the class's lowest-rank C' columns: lane j
+// of a quadrant keeps the 4*NS floats that lane j of a warp would load for that
+// column (the same float4 layout as global memory). Reads are tcgen05.ld
+// (LDTM), which bypasses the L1/shared-memory data path that the rest of the
+// loop saturates (measured on B200: ~450 B/clk/SM vs 128 for LDS.128).
+// ---------------------------------------------------------------------------
+template <int NS> struct TmemShape;  // 32x32b.x(4*NS): 4*NS consecutive columns per lane
+#define TQSB_TM_REGS16(P) P(0) P(1) P(2) P(3)
+template <int NS>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float4 (&c)[NS]) {
+    uint32_t r[4 * NS];
+    if constexpr (NS == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {"
+            "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+            "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+            "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+              "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]),
+              "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),
+              "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+              "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]),
+              "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]),
+              "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+            : "r"(taddr));
+    } else if constexpr (NS == 8) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {"
+            "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+              "=r"(r[31])
+            : "r"(taddr));
+    } else if constexpr (NS == 4) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {"
+            "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    } else if constexpr (NS == 2) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                       "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+    } else {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(taddr));
+    }
+#pragma unroll
+    for (int i = 0; i < NS; ++i)
+        c[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                           __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// store 4 columns (one float4) per call: 32x32b.x4
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, float4 v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+                 "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+                 "r"(__float_as_uint(v.w))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_sync_all() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// per-warp scratch floats: the init transpose buffer zbuf[gamma][sigma] (float2,
+// row stride 18) / half-spectrum r0buf[sigma][rho], aliased with the element-score
+// buffer sbuf[lane][2*NS] (row stride kSbufStride floats)
 template <int W>
 struct Scratch {
-    static constexpr int kHalf = W / 2 + 1;
-    static constexpr int kZ = 32 * 18 * 2;           // zbuf[gamma][sigma] (float2), stride 18
-    static constexpr int kR = kHalf * 32 * 2;        // r0buf[sigma][rho] (float2)
-    static constexpr int kS = 32 * kSbufStride;      // sbuf[lane][slot]
+    static constexpr int kZ = 32 * 18 * 2;
+    static constexpr int kR = (W / 2 + 1) * 32 * 2;
+    static constexpr int kS = 32 * kSbufStride;
     static constexpr int kFloats = (kZ > kR ? (kZ > kS ? kZ : kS) : (kR > kS ? kR : kS));
 };
 
@@ -139,47 +233,74 @@ template <int NS, int W, int PPL>
 __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs a) {
     extern __shared__ __align__(16) float smem[];
     constexpr int COLF4 = NS * 32;  // float4 per column
+    constexpr int KP = NS * 64;     // padded frequency count
     constexpr int SCR = Scratch<W>::kFloats;
-    float4* hot = reinterpret_cast<float4*>(smem);
-    float2* unit = reinterpret_cast<float2*>(smem + size_t(a.hot) * COLF4 * 4);
-    float* scr_all = smem + size_t(a.hot) * COLF4 * 4 + 2 * 32;
+    // KP x (gamma/(s_u D_u) bits, flat k) per rank u
+    int2* s_meta = reinterpret_cast<int2*>(smem);
+    float2* unit = reinterpret_cast<float2*>(s_meta + KP);   // W (cos, sin)
+    float* scr_all = reinterpret_cast<float*>(unit + 32);
     __shared__ int s_cls;
+    __shared__ uint32_t s_tmem;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* scr = scr_all + warp * SCR;
     float2* zbuf = reinterpret_cast<float2*>(scr);
-    float* sbuf = scr;
+    float* srow = scr + lane * kSbufStride;  // this lane's element scores
 
-    if (threadIdx.x < W) unit[threadIdx.x] = make_float2(a.wc.unit32[2 * threadIdx.x],
-                                                         a.wc.unit32[2 * threadIdx.x + 1]);
+    if (threadIdx.x < W)
+        unit[threadIdx.x] = make_float2(a.wc.unit32[2 * threadIdx.x], a.wc.unit32[2 * threadIdx.x + 1]);
+    for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].y = a.wc.perm[r];
     if (threadIdx.x == 0) s_cls = -1;
-    __syncthreads();
+    // TMEM tier: a.hot columns x 4*NS TMEM columns per quadrant (512 max)
+    const int hotn = a.hot;
+    if (hotn > 0 && warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            static_cast<unsigned>(__cvta_generic_to_shared(&s_tmem))));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tmem_sync_all();
+    const uint32_t tq = hotn > 0 ? s_tmem + (uint32_t(32 * (warp & 3)) << 16) : 0u;
 
+    // synthesis pixels of this lane: p = lane + 32 j of the B x B block (loop invariant)
     const int B = a.block;
     const int nb2 = B * B;
+    int p_r[PPL], p_c[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) {
+        const int p = lane + 32 * j;
+        p_r[j] = p < nb2 ? p / B : -1;
+        p_c[j] = p < nb2 ? p % B : 0;
+    }
 
     for (int it_item = blockIdx.x; it_item < a.n_items; it_item += gridDim.x) {
         const WorkItem item = a.items[it_item];
-        if (item.cls != s_cls) {  // CTA-uniform: refill the hot-column cache
-            __syncthreads();
+        if (item.cls != s_cls) {  // CTA-uniform: refill the class's on-chip tables
+            tmem_sync_all();
             const float4* src = reinterpret_cast<const float4*>(a.tabs[item.cls].cpack);
-            const int n = a.hot * COLF4;
-            for (int i = threadIdx.x; i < n; i += blockDim.x) hot[i] = __ldg(src + i);
-            __syncthreads();
+            if (warp < 4) {  // one warp per TMEM lane quadrant copies the hot columns
+                for (int j = 0; j < hotn; ++j) {
+#pragma unroll
+                    for (int i = 0; i < NS; ++i)
+                        tmem_st4(tq + uint32_t(j * 4 * NS + 4 * i), __ldg(src + size_t(j) * COLF4 + i * 32 + lane));
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            const float* fsrc = a.tabs[item.cls].fac;
+            for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].x = __float_as_int(__ldg(fsrc + r));
+            tmem_sync_all();
             if (threadIdx.x == 0) s_cls = item.cls;
             __syncthreads();
         }
-        const ClassTab& ct = a.tabs[item.cls];
-        const float4* gcols = reinterpret_cast<const float4*>(ct.cpack);
-        const float2* scale2 = reinterpret_cast<const float2*>(ct.scale);
+        const ClassTab ct = a.tabs[item.cls];
+        const float4* __restrict__ gcols = reinterpret_cast<const float4*>(ct.cpack);
+        const float2* __restrict__ scale2 = reinterpret_cast<const float2*>(ct.scale);
 
         for (int ti = item.start + warp; ti < item.start + item.count; ti += kWarpsF32) {
             const Task tk = a.tasks[ti];
             // ---------------- init: window image column per lane ----------------
             float colv[W];
             {
-                const int gc = tk.origin_col + lane;
-                int fc = gc >> 1;
+                int fc = (tk.origin_col + lane) >> 1;
                 fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
 #pragma unroll
                 for (int eta = 0; eta < W; ++eta) {
@@ -215,11 +336,10 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             for (int sg = 0; sg < H; ++sg) r0[sg] = make_float2(0.f, 0.f);
 #pragma unroll 4
             for (int g = 0; g < W; ++g) {
-                const float2 u = unit[(g * lane) % W];  // conj: (u.x, -u.y)
+                const float2 u = unit[(g * lane) % W];
 #pragma unroll
                 for (int sg = 0; sg < H; ++sg) {
                     const float2 z = zbuf[g * 18 + sg];
-                    // (z.x + i z.y)(u.x - i u.y)
                     r0[sg].x = fmaf(z.x, u.x, fmaf(z.y, u.y, r0[sg].x));
                     r0[sg].y = fmaf(z.y, u.x, fmaf(-z.x, u.y, r0[sg].y));
                 }
@@ -231,7 +351,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 for (int sg = 0; sg < H; ++sg) r0buf[sg * W + lane] = r0[sg];
             }
             __syncwarp();
-            // gather into rank order, scale, first scores
+            // gather into rank order and scale: R'_r = s_r R0[perm r]
             float4 R[NS];
 #pragma unroll
             for (int i = 0; i < NS; ++i) {
@@ -241,15 +361,13 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 float2 v0 = r0buf[s0 & 0xffff], v1 = r0buf[s1 & 0xffff];
                 if (s0 & (1 << 30)) v0.y = -v0.y;
                 if (s1 & (1 << 30)) v1.y = -v1.y;
-                float2 re = make_float2(v0.x, v1.x), im = make_float2(v0.y, v1.y);
-                re = __fmul2_rn(sc, re);
-                im = __fmul2_rn(sc, im);
+                const float2 re = __fmul2_rn(sc, make_float2(v0.x, v1.x));
+                const float2 im = __fmul2_rn(sc, make_float2(v0.y, v1.y));
                 R[i] = make_float4(re.x, re.y, im.x, im.y);
             }
             __syncwarp();
-            float lmax = score_pass<NS>(R, lane, sbuf);
+            float lmax = score_pass<NS>(R, srow);
 
-            // synthesis accumulators: pixel p = lane + 32 j of the B x B block
             float acc[PPL];
 #pragma unroll
             for (int j = 0; j < PPL; ++j) acc[j] = 0.f;
@@ -260,65 +378,66 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             for (; it < a.iterations; ++it) {
                 __syncwarp();
                 // ---- argmax over the warp (NaN = inadmissible, ignored by max) ----
-                float gmax = lmax;
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1)
-                    gmax = fmaxf(gmax, __shfl_xor_sync(FULL, gmax, off));
+                const float gmax = warp_max_f32(lmax);
                 if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
                 const unsigned cand = __ballot_sync(FULL, lmax == gmax);
-                const int L0 = __ffs(cand) - 1;
-                const float sv = lane < NS ? sbuf[L0 * kSbufStride + lane] : qnan();
-                const unsigned sm = __ballot_sync(FULL, sv == gmax);
-                int u, Lw, slot, b;
-                float4 v;
-                if (__popc(cand) == 1 && __popc(sm) == 1) {
-                    Lw = L0;
-                    slot = __ffs(sm) - 1;
-                    v = pick_slot<NS>(R, slot);
-                    const float e0 = fmaf(v.z, v.z, v.x * v.x);
-                    const float e1 = fmaf(v.w, v.w, v.y * v.y);
-                    const int b0 = e0 == gmax, b1 = e1 == gmax;
-                    int bb = b0 ? 0 : 1;
-                    if (b0 && b1) {
-                        const int r0i = 64 * slot + 2 * lane;
-                        bb = __ldg(a.wc.perm + r0i) < __ldg(a.wc.perm + r0i + 1) ? 0 : 1;
-                    }
-                    b = __shfl_sync(FULL, bb, Lw);
-                    u = 64 * slot + 2 * Lw + b;
+                int Lw = __ffs(cand) - 1;
+                const float sv = lane < 2 * NS ? scr[Lw * kSbufStride + lane] : qnan();
+                const unsigned hit = __ballot_sync(FULL, sv == gmax);
+                int t;  // element index within lane Lw: slot t>>1, half t&1
+                if (__popc(cand) == 1 && __popc(hit) == 1) {
+                    t = __ffs(hit) - 1;
                 } else {
-                    // general tie path: smallest flat index among all maxima
+                    // ties: smallest flat index among all maxima (rljsde.cpp:147-156)
                     unsigned key = 0xffffffffu;
 #pragma unroll
-                    for (int i = 0; i < NS; ++i) {
-                        const float e0 = fmaf(R[i].z, R[i].z, R[i].x * R[i].x);
-                        const float e1 = fmaf(R[i].w, R[i].w, R[i].y * R[i].y);
-                        const int r = 64 * i + 2 * lane;
-                        if (e0 == gmax) key = min(key, (unsigned(__ldg(a.wc.perm + r)) << 12) | r);
-                        if (e1 == gmax)
-                            key = min(key, (unsigned(__ldg(a.wc.perm + r + 1)) << 12) | (r + 1));
+                    for (int e = 0; e < 2 * NS; ++e) {
+                        if (srow[e] == gmax) {
+                            const int r = 64 * (e >> 1) + 2 * lane + (e & 1);
+                            key = min(key, (unsigned(s_meta[r].y) << 16) | unsigned(r));
+                        }
                     }
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1)
                         key = min(key, __shfl_xor_sync(FULL, key, off));
-                    u = key & 0xfff;
-                    slot = u >> 6;
-                    Lw = (u >> 1) & 31;
-                    b = u & 1;
-                    v = pick_slot<NS>(R, slot);
+                    const int r = int(key & 0xffffu);
+                    Lw = (r >> 1) & 31;
+                    t = 2 * (r >> 6) + (r & 1);
                 }
-                const float ure = __shfl_sync(FULL, b ? v.y : v.x, Lw);
-                const float uim = __shfl_sync(FULL, b ? v.w : v.z, Lw);
-                const float f = __ldg(ct.fac + u);
+                const int slot = t >> 1, b = t & 1;
+                const int u = 64 * slot + 2 * Lw + b;
+                // ---- issue the whole C' column now; its latency overlaps the pick ----
+                constexpr int PF = NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH;
+                float4 c[NS];
+                const float4* col = gcols + size_t(u) * COLF4;
+                const bool in_tmem = u < hotn;
+                if (in_tmem) {
+                    tmem_ld<NS>(tq + uint32_t(u * 4 * NS), c);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
+                }
+                const float2 v = pick_elem<NS>(R, t);
+                const float ure = __shfl_sync(FULL, v.x, Lw);
+                const float uim = __shfl_sync(FULL, v.y, Lw);
+                const int2 meta = s_meta[u];  // (fac bits, flat k) of rank u
+                const float f = __int_as_float(meta.x);
                 const float gre = f * ure, gim = f * uim;
-                const int kflat = __ldg(a.wc.perm + u);
+                const int kflat = meta.y;
+                __syncwarp();  // all score reads of this iteration precede the rewrite
+                if (in_tmem) {
+                    tmem_wait_ld();
+                    lmax = update_pass<NS, NS>(R, c, col, lane, gre, gim, srow);
+                } else {
+                    lmax = update_pass<NS, PF>(R, c, col, lane, gre, gim, srow);
+                }
+                // ---- synthesis of the kept block pixels (off the critical path) ----
                 const int sigma = kflat / W, rho = kflat % W;
-                // ---- synthesis of the kept block pixels ----
 #pragma unroll
                 for (int j = 0; j < PPL; ++j) {
-                    const int p = lane + 32 * j;
-                    if (p < nb2) {
-                        const int eta = rw + p / B, gam = cw + p % B;
-                        const float2 ph = unit[(eta * sigma + gam * rho) % W];
+                    if (p_r[j] >= 0) {
+                        const int idx = ((rw + p_r[j]) * sigma + (cw + p_c[j]) * rho) % W;
+                        const float2 ph = unit[idx];
                         acc[j] = fmaf(gre, ph.x, fmaf(-gim, ph.y, acc[j]));
                     }
                 }
@@ -327,17 +446,12 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                     a.trace_gd[2 * it] = gre;
                     a.trace_gd[2 * it + 1] = gim;
                 }
-                // ---- rank-1 update streamed from C'[:,u], fused with the next scores ----
-                __syncwarp();  // locate reads of sbuf complete before it is rewritten
-                const float4* col = (u < a.hot ? hot : gcols) + size_t(u) * COLF4;
-                lmax = update_pass<NS>(R, col, lane, gre, gim, sbuf);
             }
             // ---- placement: clip + crop straight into the output ----
 #pragma unroll
             for (int j = 0; j < PPL; ++j) {
-                const int p = lane + 32 * j;
-                if (p < nb2) {
-                    const int orow = tk.block_row + p / B, ocol = tk.block_col + p % B;
+                if (p_r[j] >= 0) {
+                    const int orow = tk.block_row + p_r[j], ocol = tk.block_col + p_c[j];
                     if (orow < a.out_rows && ocol < a.out_cols) {
                         float val = acc[j];
                         if (a.clip) val = fminf(fmaxf(val, 0.f), 1.f);
@@ -351,19 +465,22 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                     __syncwarp();
                     for (int p = lane; p < W * W; p += 32) {
                         const int eta = p / W, gam = p % W;
-                        float s = 0.f;
-                        for (int t = 0; t < it; ++t) {
-                            const int k = a.trace_picks[t];
+                        float sacc = 0.f;
+                        for (int q = 0; q < it; ++q) {
+                            const int k = a.trace_picks[q];
                             const float2 ph = unit[(eta * (k / W) + gam * (k % W)) % W];
-                            s = fmaf(float(a.trace_gd[2 * t]), ph.x,
-                                     fmaf(-float(a.trace_gd[2 * t + 1]), ph.y, s));
+                            sacc = fmaf(float(a.trace_gd[2 * q]), ph.x,
+                                        fmaf(-float(a.trace_gd[2 * q + 1]), ph.y, sacc));
                         }
-                        a.trace_window[p] = s;
+                        a.trace_window[p] = sacc;
                     }
                 }
             }
         }
     }
+    tmem_sync_all();
+    if (hotn > 0 && warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem));
 }
 
 template <int NS, int W, int PPL>
@@ -398,18 +515,16 @@ int launch_w(const SolveArgs& a, int n_slots, cudaStream_t s, int num_sms) {
 } // namespace
 
 size_t solve_f32_smem_bytes(int n_slots, int hot) {
-    // hot columns + unit table + per-warp scratch (sized for W = 32, the largest)
-    return size_t(hot) * n_slots * 32 * 16 + 2 * 32 * 4 +
-           size_t(kWarpsF32) * Scratch<32>::kFloats * 4;
+    // (fac, perm) per rank + unit table + per-warp scratch; hot columns live in TMEM
+    (void)hot;
+    return size_t(n_slots) * 64 * 8 + 32 * 8 + size_t(kWarpsF32) * Scratch<32>::kFloats * 4;
 }
 
 int solve_f32_max_hot(int n_slots, int device) {
-    int optin = 0;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    const long base = long(solve_f32_smem_bytes(n_slots, 0)) + 64;  // static smem margin
-    const long col = long(n_slots) * 32 * 16;
-    const long h = (long(optin) - base) / col;
-    return h < 0 ? 0 : int(h);
+    // TMEM tier: 512 columns per lane quadrant, 4*NS columns per C' column
+    (void)device;
+    const int h = 512 / (4 * n_slots);
+    return h < 64 * n_slots ? h : 64 * n_slots;
 }
 
 int launch_solve_f32(const SolveArgs& a, int n_slots, void* stream, int num_sms) {

@@ -9,9 +9,12 @@
 namespace tqsb {
 
 constexpr int kMaxWindow = 32;  // device paths hold a warp-row per window row/col
-constexpr int kWarpsF32 = 12;   // warps per CTA of the fp32 solve kernel (1 CTA/SM, <=168 regs)
+#ifndef TQSB_WARPS_F32
+#define TQSB_WARPS_F32 12
+#endif
+constexpr int kWarpsF32 = TQSB_WARPS_F32;  // warps per CTA of the fp32 solve kernel (1 CTA/SM)
 constexpr int kWarpsF64 = 4;    // warps per CTA of the fp64 parity kernel
-constexpr int kSbufStride = 20; // floats per lane in the slot-max buffer (conflict-free STS.128)
+constexpr int kSbufStride = 36; // floats per lane in the element-score buffer (conflict-free STS.128)
 
 // One target block: top-left output pixel and clamped window origin
 // (BlockTask, pipeline.cpp:54-58), plus its class slot in the plan.
