@@ -81,18 +81,6 @@ def make_inputs(wl):
     return gt, pat, frame
 
 
-def band_rows(padM, B, rank, world):
-    nbr = padM // B
-    return rank * nbr // world, (rank + 1) * nbr // world
-
-
-def band_frame_rows(br0, br1, B, W, padM, frame_rows):
-    lead = (W - B) // 2
-    omin = min(max(br0 * B - lead, 0), padM - W)
-    omax = min(max((br1 - 1) * B - lead, 0), padM - W)
-    return min(omin // 2, frame_rows - 1), min(frame_rows, (omax + W - 1) // 2 + 1)
-
-
 # ---------------------------------------------------------------- CPU reference
 def run_reference_sample(wl, sample_rows, steps, warmup):
     """The unmodified reference on a strip of the workload (rows 0..sample_rows),
@@ -226,10 +214,10 @@ def main_ours(args):
     gt, pat, frame = make_inputs(wl)
     fr, fc = frame.shape
     M, N = 2 * fr, 2 * fc
-    padM = -(-M // 4) * 4
-    br0, br1 = band_rows(padM, B, rank, world)
-    f0, f1 = band_frame_rows(br0, br1, B, W, padM, fr)
-    out_r0, out_r1 = br0 * B, min(br1 * B, M)
+    from paper_2205_02646_b200 import bands
+    br0, br1 = bands.band(fr, B, rank, world)
+    f0, f1 = bands.band_frame_rows(fr, W, B, br0, br1)
+    out_r0, out_r1 = bands.band_output_rows(fr, B, br0, br1)
 
     peaks = tq.probe_peaks(local)
     plan = tq.Plan(pat, cfg, devices=[local])

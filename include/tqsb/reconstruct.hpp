@@ -1,0 +1,258 @@
+// reconstruct.hpp -- header-only C++ drop-in for the reference entry point
+//
+//   tqs::ReconstructionReport tqs::reconstruct(const MeasurementFrame&, const QuadrantPattern&,
+//                                              const ReconstructionConfig&, KernelCache* = nullptr,
+//                                              const Image* reference = nullptr);
+//   (/root/reference/proj/include/tqs/pipeline.hpp:45-47)
+//
+// The types mirror the reference's (image.hpp:10-27, grid.hpp:19-53, basis.hpp:15-18 and
+// 77-82, pipeline.hpp:17-39) field for field, so existing call sites compile against
+// namespace tqsb unchanged; the work runs on the GPU through the C ABI in tqsb.h.
+// Errors are rethrown as the reference's exception types: std::invalid_argument
+// (validation, pipeline.cpp:27-42), std::logic_error (cache window mismatch,
+// pipeline.cpp:146-147), std::runtime_error (device failures).
+//
+// KernelCache is the device-resident table store: bound to the first pattern and
+// config it sees, reused across calls (the reference's shared KernelCache,
+// pipeline.cpp:110-133), with hits()/misses() counters.
+#pragma once
+
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tqsb.h"
+
+namespace tqsb {
+
+struct Image {
+    int rows = 0;
+    int cols = 0;
+    std::vector<double> values;
+    Image() = default;
+    Image(int r, int c, double fill = 0.0) : rows(r), cols(c), values(size_t(r) * c, fill) {
+        if (r < 0 || c < 0) throw std::invalid_argument("image dimensions must be non-negative");
+    }
+    double& at(int r, int c) { return values[size_t(r) * cols + c]; }
+    double at(int r, int c) const { return values[size_t(r) * cols + c]; }
+    size_t size() const { return values.size(); }
+    bool same_size(const Image& o) const { return rows == o.rows && cols == o.cols; }
+};
+
+struct MeasurementFrame {
+    int rows = 0;
+    int cols = 0;
+    std::vector<double> values;
+    MeasurementFrame() = default;
+    MeasurementFrame(int r, int c, double fill = 0.0) : rows(r), cols(c), values(size_t(r) * c, fill) {}
+    double& at(int r, int c) { return values[size_t(r) * cols + c]; }
+    double at(int r, int c) const { return values[size_t(r) * cols + c]; }
+    size_t size() const { return values.size(); }
+};
+
+struct QuadrantPattern {
+    int period = 0;
+    uint64_t seed = 0;
+    std::string rng;
+    std::vector<uint8_t> opaque;
+    int cellsPerPeriod() const { return period / 2; }
+};
+
+enum class Precision { Single, Double };
+enum class Algorithm { Ljsde, Rljsde };
+enum class Compute { Fp32, Fp64 };  // device arithmetic (not in the reference)
+
+struct WeightingConfig {
+    double spatialDecay = 0.8;
+    double frequencyExponent = 2.0;
+};
+
+struct SolverOptions {
+    int maxIterations = 200;
+    double stepWidth = 0.5;
+    bool earlyStop = false;  // L-JSDE only in the reference; rejected here when set
+    double earlyStopScale = 1e-14;
+};
+
+struct ReconstructionConfig {
+    int window = 32;
+    int block = 4;
+    SolverOptions solver;
+    WeightingConfig weighting;
+    Precision precision = Precision::Double;
+    bool clipOutput = true;
+    Algorithm algorithm = Algorithm::Rljsde;
+    int threads = 1;
+    Compute compute = Compute::Fp32;
+    int hotColumns = -1;
+    std::vector<int> devices{0};
+};
+
+struct ReconstructionReport {
+    Image output;
+    double seconds = 0.0;
+    double warmSeconds = 0.0;
+    long blocksProcessed = 0;
+    size_t classesTotal = 0;
+    size_t classesInterior = 0;
+    size_t classesCreated = 0;
+    uint64_t cacheHits = 0;
+    uint64_t cacheMisses = 0;
+    std::optional<double> psnrDb;
+    double e2eSeconds = 0.0;
+};
+
+namespace detail {
+[[noreturn]] inline void throw_status(int rc) {
+    const std::string msg = tqsb_last_error();
+    switch (rc) {
+        case TQSB_EINVAL: throw std::invalid_argument(msg);
+        case TQSB_ELOGIC: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+inline void check(int rc) {
+    if (rc != TQSB_OK) throw_status(rc);
+}
+inline tqsb_config to_c(const ReconstructionConfig& c) {
+    tqsb_config k;
+    tqsb_config_default(&k);
+    k.window = c.window;
+    k.block = c.block;
+    k.max_iterations = c.solver.maxIterations;
+    k.step_width = c.solver.stepWidth;
+    k.spatial_decay = c.weighting.spatialDecay;
+    k.frequency_exponent = c.weighting.frequencyExponent;
+    k.precision = c.precision == Precision::Double ? TQSB_PRECISION_DOUBLE : TQSB_PRECISION_SINGLE;
+    k.clip_output = c.clipOutput ? 1 : 0;
+    k.threads = c.threads;
+    k.compute = c.compute == Compute::Fp64 ? TQSB_COMPUTE_FP64 : TQSB_COMPUTE_FP32;
+    k.hot_columns = c.hotColumns;
+    return k;
+}
+}  // namespace detail
+
+// Device-resident kernel store (the reference's KernelCache, rljsde.hpp:81-100).
+class KernelCache {
+public:
+    KernelCache() = default;
+    KernelCache(const KernelCache&) = delete;
+    KernelCache& operator=(const KernelCache&) = delete;
+    ~KernelCache() { clear(); }
+
+    size_t classCount() const {
+        long long n = 0;
+        if (plan_) tqsb_plan_stats(plan_, &n, nullptr);
+        return size_t(n);
+    }
+    uint64_t hits() const { return hits_; }
+    uint64_t misses() const { return misses_; }
+    void resetStats() { hits_ = misses_ = 0; }
+    void clear() {
+        if (plan_) tqsb_plan_destroy(plan_);
+        plan_ = nullptr;
+        window_ = 0;
+    }
+
+    // internal: bind on first use; a different window is the reference's logic_error
+    tqsb_plan* bind(const QuadrantPattern& p, const ReconstructionConfig& c) {
+        if (plan_) {
+            if (window_ != c.window)
+                throw std::logic_error("kernel cache holds a different window size");
+            return plan_;
+        }
+        const tqsb_config k = detail::to_c(c);
+        detail::check(tqsb_plan_create(p.opaque.data(), p.period, &k, c.devices.data(),
+                                       int(c.devices.size()), &plan_));
+        window_ = c.window;
+        return plan_;
+    }
+    void count(uint64_t h, uint64_t m) {
+        hits_ += h;
+        misses_ += m;
+    }
+
+private:
+    tqsb_plan* plan_ = nullptr;
+    int window_ = 0;
+    uint64_t hits_ = 0, misses_ = 0;
+};
+
+inline ReconstructionReport reconstruct(const MeasurementFrame& frame, const QuadrantPattern& pattern,
+                                        const ReconstructionConfig& config,
+                                        KernelCache* cache = nullptr,
+                                        const Image* reference = nullptr) {
+    const tqsb_config k = detail::to_c(config);
+    detail::check(tqsb_validate_config(&k, pattern.period));
+    if (config.algorithm != Algorithm::Rljsde)
+        throw std::invalid_argument("only the RL-JSDE algorithm runs on the device");
+    if (frame.rows < 1 || frame.cols < 1) throw std::invalid_argument("empty measurement frame");
+    if (reference && (reference->rows != 2 * frame.rows || reference->cols != 2 * frame.cols))
+        throw std::invalid_argument("reference dimensions do not match the reconstruction");
+    KernelCache local;
+    KernelCache* kc = cache ? cache : &local;
+    tqsb_plan* plan = kc->bind(pattern, config);
+    ReconstructionReport rep;
+    rep.output = Image(2 * frame.rows, 2 * frame.cols);
+    tqsb_report r;
+    detail::check(tqsb_reconstruct(plan, frame.values.data(), frame.rows, frame.cols,
+                                   rep.output.values.data(),
+                                   reference ? reference->values.data() : nullptr, &r));
+    rep.seconds = r.seconds;
+    rep.warmSeconds = r.warm_seconds;
+    rep.e2eSeconds = r.e2e_seconds;
+    rep.blocksProcessed = long(r.blocks_processed);
+    rep.classesTotal = size_t(r.classes_total);
+    rep.classesInterior = size_t(r.classes_interior);
+    rep.classesCreated = size_t(r.classes_created);
+    rep.cacheHits = uint64_t(r.cache_hits);
+    rep.cacheMisses = uint64_t(r.cache_misses);
+    if (r.has_psnr) rep.psnrDb = r.psnr_db;
+    kc->count(rep.cacheHits, rep.cacheMisses);
+    return rep;
+}
+
+// generate_pattern (grid.cpp:8-26)
+inline QuadrantPattern generate_pattern(uint64_t seed, int period, int blockSize = 4) {
+    QuadrantPattern p;
+    p.period = period;
+    p.seed = seed;
+    p.rng = "mt19937_64";
+    if (period < 4 || period % 2 != 0)
+        throw std::invalid_argument("pattern period must be even and >= 4");
+    p.opaque.resize(size_t(period / 2) * (period / 2));
+    detail::check(tqsb_generate_pattern(seed, period, blockSize, p.opaque.data()));
+    return p;
+}
+
+// simulate_measurement (grid.cpp:46-66)
+inline MeasurementFrame simulate_measurement(const Image& image, const QuadrantPattern& pattern) {
+    if (image.rows % 2 != 0 || image.cols % 2 != 0)
+        throw std::invalid_argument("image dimensions must be even");
+    MeasurementFrame f(image.rows / 2, image.cols / 2);
+    detail::check(tqsb_simulate(image.values.data(), image.rows, image.cols,
+                                pattern.opaque.data(), pattern.period, f.values.data()));
+    return f;
+}
+
+// psnr (pipeline.cpp:221-233)
+inline double psnr(const Image& reference, const Image& estimate) {
+    if (!reference.same_size(estimate)) throw std::invalid_argument("psnr: dimension mismatch");
+    return tqsb_psnr(reference.values.data(), estimate.values.data(),
+                     (long long)reference.values.size());
+}
+
+namespace testing {
+// tests/support/synthetic.cpp:9-80
+inline Image synthetic_image(int rows, int cols, uint64_t seed) {
+    Image img(rows, cols);
+    detail::check(tqsb_synthetic_image(rows, cols, seed, img.values.data()));
+    return img;
+}
+}  // namespace testing
+
+}  // namespace tqsb

@@ -1,0 +1,160 @@
+// C++ drop-in check: the reference's pipeline test cases (test_pipeline.cpp) written
+// against include/tqsb/reconstruct.hpp -- the same call shapes as tqs::reconstruct,
+// the same exception types -- running on the GPU through libtqsb.so.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tqsb/reconstruct.hpp"
+
+using namespace tqsb;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                            \
+    do {                                                                       \
+        ++g_checks;                                                            \
+        if (!(cond)) {                                                         \
+            ++g_fail;                                                          \
+            std::printf("  FAILED %s:%d  %s\n", __FILE__, __LINE__, #cond);    \
+        }                                                                      \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                                               \
+    do {                                                                       \
+        ++g_checks;                                                            \
+        bool ok = false;                                                       \
+        try { (void)(expr); } catch (const T&) { ok = true; } catch (...) {}   \
+        if (!ok) { ++g_fail; std::printf("  FAILED %s:%d  %s throws %s\n", __FILE__, __LINE__, #expr, #T); } \
+    } while (0)
+
+static void run(const char* name, const std::function<void()>& f) {
+    const int before = g_fail;
+    try {
+        f();
+    } catch (const std::exception& e) {
+        ++g_fail;
+        std::printf("  EXCEPTION %s\n", e.what());
+    }
+    std::printf("[%s] %s\n", g_fail == before ? "PASS" : "FAIL", name);
+}
+
+static ReconstructionConfig test_config(int window = 16, int iterations = 30) {
+    ReconstructionConfig cfg;
+    cfg.window = window;
+    cfg.block = 4;
+    cfg.solver.maxIterations = iterations;
+    cfg.clipOutput = false;
+    cfg.threads = 1;
+    return cfg;
+}
+
+int main() {
+    run("configuration validation (test_pipeline.cpp:105-147)", [] {
+        const QuadrantPattern p = generate_pattern(7, 32);
+        const Image img = testing::synthetic_image(64, 64, 4);
+        const MeasurementFrame f = simulate_measurement(img, p);
+        auto expectThrow = [&](ReconstructionConfig cfg) {
+            CHECK_THROWS_AS(reconstruct(f, p, cfg), std::invalid_argument);
+        };
+        ReconstructionConfig cfg = test_config(); cfg.window = 7; expectThrow(cfg);
+        cfg = test_config(); cfg.block = 3; expectThrow(cfg);
+        cfg = test_config(6); cfg.block = 3; expectThrow(cfg);
+        cfg = test_config(); cfg.solver.maxIterations = -1; expectThrow(cfg);
+        cfg = test_config(); cfg.solver.stepWidth = 0.0; expectThrow(cfg);
+        cfg = test_config(); cfg.solver.stepWidth = 1.5; expectThrow(cfg);
+        cfg = test_config(); cfg.threads = -2; expectThrow(cfg);
+        const QuadrantPattern p6 = generate_pattern(3, 6, 2);
+        CHECK_THROWS_AS(reconstruct(f, p6, test_config()), std::invalid_argument);
+        const Image tiny = testing::synthetic_image(16, 16, 5);
+        const MeasurementFrame tf = simulate_measurement(tiny, p);
+        CHECK_THROWS_AS(reconstruct(tf, p, test_config(32)), std::invalid_argument);
+        CHECK_THROWS_AS(reconstruct(MeasurementFrame(), p, test_config()), std::invalid_argument);
+    });
+
+    run("block tiling covers the frame exactly (test_pipeline.cpp:149-167)", [] {
+        const QuadrantPattern p = generate_pattern(7, 32);
+        const Image img(64, 64, 0.6);
+        const MeasurementFrame f = simulate_measurement(img, p);
+        ReconstructionConfig cfg = test_config(16, 1);
+        cfg.solver.stepWidth = 1.0;
+        cfg.compute = Compute::Fp64;
+        const ReconstructionReport report = reconstruct(f, p, cfg, nullptr, &img);
+        CHECK(report.blocksProcessed == 256);
+        CHECK(report.output.rows == 64 && report.output.cols == 64);
+        bool all = true;
+        for (double v : report.output.values) all = all && std::abs(v - 0.6) <= 0.6 * 1e-10;
+        CHECK(all);
+        CHECK(report.psnrDb.has_value() && *report.psnrDb >= 60.0);
+    });
+
+    run("offset class accounting on an aligned image (test_pipeline.cpp:169-190)", [] {
+        const QuadrantPattern p = generate_pattern(7, 32);
+        const Image img = testing::synthetic_image(64, 64, 6);
+        const MeasurementFrame f = simulate_measurement(img, p);
+        const ReconstructionReport r32 = reconstruct(f, p, test_config(32, 2));
+        CHECK(r32.classesInterior == 64);
+        CHECK(r32.classesTotal == 81);
+        CHECK(r32.classesCreated == 81);
+        CHECK(r32.cacheMisses == 81);
+        CHECK(r32.cacheHits == 256);
+        const ReconstructionReport r16 = reconstruct(f, p, test_config(16, 2));
+        CHECK(r16.classesInterior == 64);
+        CHECK(r16.classesTotal == 100);
+    });
+
+    run("external kernel cache is reused across runs (test_pipeline.cpp:192-217)", [] {
+        const QuadrantPattern p = generate_pattern(7, 32);
+        const Image img = testing::synthetic_image(64, 64, 7);
+        const MeasurementFrame f = simulate_measurement(img, p);
+        ReconstructionConfig cfg = test_config(16, 3);
+        KernelCache cache;
+        const ReconstructionReport first = reconstruct(f, p, cfg, &cache);
+        CHECK(first.classesCreated == first.classesTotal);
+        CHECK(cache.classCount() == first.classesTotal);
+        const ReconstructionReport second = reconstruct(f, p, cfg, &cache);
+        CHECK(second.classesCreated == 0);
+        CHECK(second.cacheMisses == 0);
+        CHECK(second.output.values == first.output.values);
+        CHECK_THROWS_AS(reconstruct(f, p, test_config(32, 3), &cache), std::logic_error);
+    });
+
+    run("outputs are bitwise reproducible across runs (test_pipeline.cpp:238-262)", [] {
+        const QuadrantPattern p = generate_pattern(11, 32);
+        const Image img = testing::synthetic_image(64, 64, 9);
+        const MeasurementFrame f = simulate_measurement(img, p);
+        const ReconstructionConfig cfg = test_config(16, 25);
+        const ReconstructionReport a = reconstruct(f, p, cfg);
+        const ReconstructionReport b = reconstruct(f, p, cfg);
+        CHECK(a.output.values == b.output.values);
+    });
+
+    run("clipping bounds the output to the display range (test_pipeline.cpp:264-276)", [] {
+        const QuadrantPattern p = generate_pattern(7, 32);
+        const Image img = testing::synthetic_image(64, 64, 10);
+        const MeasurementFrame f = simulate_measurement(img, p);
+        ReconstructionConfig cfg = test_config(16, 40);
+        cfg.clipOutput = true;
+        const ReconstructionReport report = reconstruct(f, p, cfg);
+        bool ok = true;
+        for (double v : report.output.values) ok = ok && v >= 0.0 && v <= 1.0;
+        CHECK(ok);
+    });
+
+    run("production defaults beat nearest-neighbour upsampling", [] {
+        const QuadrantPattern p = generate_pattern(7, 8);
+        const Image img = testing::synthetic_image(128, 128, 301);
+        const MeasurementFrame f = simulate_measurement(img, p);
+        ReconstructionConfig cfg;  // W=32 B=4 nu=200 gamma=0.5, clip on, fp32
+        const ReconstructionReport r = reconstruct(f, p, cfg, nullptr, &img);
+        Image nn(128, 128);
+        for (int y = 0; y < 128; ++y)
+            for (int x = 0; x < 128; ++x) nn.at(y, x) = f.at(y / 2, x / 2);
+        CHECK(r.psnrDb.has_value() && *r.psnrDb > psnr(img, nn));
+        CHECK(r.blocksProcessed == 1024 && r.classesTotal == 9);
+    });
+
+    std::printf("%d checks, %d failures\n", g_checks, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
