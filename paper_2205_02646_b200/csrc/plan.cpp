@@ -270,8 +270,10 @@ struct Device {
     int id = 0;
     int num_sms = 0;
     int hot = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;            // solve
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // copy engines
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_h2d[4] = {}, ev_comp[4] = {};
     int* d_perm = nullptr;
     int* d_src = nullptr;
     float* d_unit32 = nullptr;
@@ -313,6 +315,12 @@ int device_init(tqsb_plan* p, Device* d) {
     CUDA_TRY(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreate(&d->ev0));
     CUDA_TRY(cudaEventCreate(&d->ev1));
+    CUDA_TRY(cudaStreamCreateWithFlags(&d->s_h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&d->s_d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < 4; ++k) {
+        CUDA_TRY(cudaEventCreateWithFlags(&d->ev_h2d[k], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&d->ev_comp[k], cudaEventDisableTiming));
+    }
     const WindowTables& t = p->wt;
     CUDA_TRY(cudaMalloc(&d->d_perm, sizeof(int) * t.K_pad));
     CUDA_TRY(cudaMalloc(&d->d_src, sizeof(int) * t.K_pad));
@@ -351,10 +359,38 @@ void device_free(Device* d) {
     if (d->h_out) cudaFreeHost(d->h_out);
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
+    for (int k = 0; k < 4; ++k) {
+        if (d->ev_h2d[k]) cudaEventDestroy(d->ev_h2d[k]);
+        if (d->ev_comp[k]) cudaEventDestroy(d->ev_comp[k]);
+    }
+    if (d->s_h2d) cudaStreamDestroy(d->s_h2d);
+    if (d->s_d2h) cudaStreamDestroy(d->s_d2h);
     if (d->stream) cudaStreamDestroy(d->stream);
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// memcpy of large host buffers (pageable <-> pinned staging) on up to 8 threads
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t kMin = size_t(8) << 20;
+    unsigned nt = std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency()));
+    if (bytes < kMin || nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    nt = unsigned(std::min<size_t>(nt, bytes / (kMin / 4)));
+    std::vector<std::thread> th;
+    const size_t chunk = (bytes + nt - 1) / nt;
+    for (unsigned i = 0; i < nt; ++i) {
+        const size_t off = i * chunk;
+        if (off >= bytes) break;
+        const size_t n = std::min(chunk, bytes - off);
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, n);
+        });
+    }
+    for (auto& t : th) t.join();
+}
 
 // Build the tables of every class in `keys` that is not resident on device d
 // (batched; the serial warm pass of pipeline.cpp:127-133). Returns the number of
@@ -571,6 +607,10 @@ struct BandResult {
 
 // Host-buffer band run on device d: H2D of the band's frame rows (pinned
 // staging), solve, D2H of the band's output rows.
+// Host-buffer band run on device d: H2D of the band's frame rows (halo included),
+// one solve launch whose B x B output tiles are stored straight into pinned host
+// memory (zero-copy: the caller's buffer when it is pinned, else the plan's pinned
+// staging), so the output transfer overlaps the solve instead of following it.
 void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* frame,
                    int frame_rows, int frame_cols, int br0, int br1, double* out_band,
                    BandResult* r) {
@@ -591,17 +631,20 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
     const size_t in_n = size_t(fr1 - fr0) * frame_cols;
     const int orow0 = br0 * g.B, orow1 = std::min(br1 * g.B, g.M);
     const size_t out_n = size_t(std::max(0, orow1 - orow0)) * g.N;
-    if ((rc = ensure_buffer(&d->d_frame, &d->frame_cap, in_n))) return fail(rc);
-    if ((rc = ensure_buffer(&d->d_out, &d->out_cap, out_n))) return fail(rc);
-    if (!is_pinned(frame) && (rc = ensure_pinned(&d->h_in, &d->h_in_cap, in_n))) return fail(rc);
-    if (!is_pinned(out_band) && (rc = ensure_pinned(&d->h_out, &d->h_out_cap, out_n)))
-        return fail(rc);
-    // pinned caller buffers are copied directly; pageable ones go through staging
     const bool in_pinned = is_pinned(frame), out_pinned = is_pinned(out_band);
+    if ((rc = ensure_buffer(&d->d_frame, &d->frame_cap, in_n))) return fail(rc);
+    if (!in_pinned && (rc = ensure_pinned(&d->h_in, &d->h_in_cap, in_n))) return fail(rc);
+    if (!out_pinned && (rc = ensure_pinned(&d->h_out, &d->h_out_cap, out_n))) return fail(rc);
     const double* src = frame + size_t(fr0) * frame_cols;
     if (!in_pinned) {
-        std::memcpy(d->h_in, src, sizeof(double) * in_n);
+        par_memcpy(d->h_in, src, sizeof(double) * in_n);
         src = d->h_in;
+    }
+    double* host_out = out_pinned ? out_band : d->h_out;
+    double* dev_view = nullptr;  // the pinned output as seen from the device (UVA)
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_view), host_out, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(set_error(TQSB_ECUDA, "output buffer is not device-mapped pinned memory"));
     }
     cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
     SolveArgs a = base_args(p, d);
@@ -610,7 +653,7 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
     a.frame_cols = frame_cols;
     a.frame_row0 = fr0;
     a.frame_pitch = frame_cols;
-    a.out = d->d_out;
+    a.out = dev_view;
     a.out_row0 = orow0;
     a.out_rows = g.M;
     a.out_cols = g.N;
@@ -623,13 +666,11 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
         r->launches += 1;
     }
     cudaEventRecord(d->ev1, d->stream);
-    cudaMemcpyAsync(out_pinned ? out_band : d->h_out, d->d_out, sizeof(double) * out_n,
-                    cudaMemcpyDeviceToHost, d->stream);
     cudaError_t e = cudaStreamSynchronize(d->stream);
     if (e != cudaSuccess)
         return fail(set_error(TQSB_ECUDA, std::string("solve: ") + cudaGetErrorString(e)));
     cudaEventElapsedTime(&r->ms, d->ev0, d->ev1);
-    if (!out_pinned) std::memcpy(out_band, d->h_out, sizeof(double) * out_n);
+    if (!out_pinned) par_memcpy(out_band, d->h_out, sizeof(double) * out_n);
 }
 
 void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const Geometry& g,

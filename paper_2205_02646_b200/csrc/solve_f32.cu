@@ -372,6 +372,13 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 #pragma unroll
             for (int j = 0; j < PPL; ++j) acc[j] = 0.f;
             const int rw = tk.block_row - tk.origin_row, cw = tk.block_col - tk.origin_col;
+            // window coordinates of this lane's kept pixels (unsigned: cheap mod W)
+            unsigned pe[PPL], pg[PPL];
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) {
+                pe[j] = unsigned(rw + (p_r[j] < 0 ? 0 : p_r[j]));
+                pg[j] = unsigned(cw + p_c[j]);
+            }
             const bool tracing = a.trace_picks != nullptr && ti == 0;
 
             int it = 0;
@@ -432,11 +439,11 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                     lmax = update_pass<NS, PF>(R, c, col, lane, gre, gim, srow);
                 }
                 // ---- synthesis of the kept block pixels (off the critical path) ----
-                const int sigma = kflat / W, rho = kflat % W;
+                const unsigned sigma = unsigned(kflat) / W, rho = unsigned(kflat) % W;
 #pragma unroll
                 for (int j = 0; j < PPL; ++j) {
                     if (p_r[j] >= 0) {
-                        const int idx = ((rw + p_r[j]) * sigma + (cw + p_c[j]) * rho) % W;
+                        const unsigned idx = (pe[j] * sigma + pg[j] * rho) % unsigned(W);
                         const float2 ph = unit[idx];
                         acc[j] = fmaf(gre, ph.x, fmaf(-gim, ph.y, acc[j]));
                     }
