@@ -22,7 +22,8 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["tables.cu", "solve_f32.cu", "solve_f64.cu", "probe.cu"]
 CPP = ["plan.cpp"]
-HEADERS = [os.path.join(CSRC, "tqsb_internal.hpp"), os.path.join(INCLUDE, "tqsb", "tqsb.h"),
+HEADERS = [os.path.join(CSRC, "tqsb_internal.hpp"), os.path.join(CSRC, "solve_common.cuh"),
+           os.path.join(INCLUDE, "tqsb", "tqsb.h"),
            os.path.abspath(__file__)]
 
 

@@ -28,195 +28,12 @@
 #include <cstdint>
 
 #include "tqsb_internal.hpp"
+#include "solve_common.cuh"
 
 namespace tqsb {
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
-
-#ifndef TQSB_PREFETCH
-#define TQSB_PREFETCH 16  // C' slots in flight ahead of the update (register budget)
-#endif
-
-__device__ __forceinline__ float qnan() { return __int_as_float(0x7fc00000); }
-
-// STS.64 straight from an FFMA2 register pair (inline PTX keeps ptxas from fusing
-// neighbouring stores into an STS.128 that needs register copies to pack)
-__device__ __forceinline__ void st_shared_f2(float* p, float2 v) {
-    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(
-                     static_cast<unsigned>(__cvta_generic_to_shared(p))),
-                 "f"(v.x), "f"(v.y)
-                 : "memory");
-}
-
-// warp-wide max in one CREDUX (redux.sync .f32, sm_100a); NaN inputs are ignored,
-// so the result is NaN only when every lane holds NaN (no admissible frequency)
-__device__ __forceinline__ float warp_max_f32(float x) {
-    float m;
-    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(m) : "f"(x));
-    return m;
-}
-
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-    float d;
-    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-    return d;
-}
-
-// (re, im) of element t (slot t>>1, half t&1) of this lane's residual; t is
-// warp-uniform, so the switch is a uniform branch, not a local-memory array.
-template <int NS>
-__device__ __forceinline__ float2 pick_elem(const float4 (&R)[NS], int t) {
-    float re = 0.f, im = 0.f;
-    switch (t) {
-#define TQSB_CASE(n)                                                            \
-    case n:                                                                     \
-        if ((n >> 1) < NS) {                                                    \
-            re = (n & 1) ? R[(n >> 1) < NS ? (n >> 1) : 0].y : R[(n >> 1) < NS ? (n >> 1) : 0].x; \
-            im = (n & 1) ? R[(n >> 1) < NS ? (n >> 1) : 0].w : R[(n >> 1) < NS ? (n >> 1) : 0].z; \
-        }                                                                       \
-        break;
-        TQSB_CASE(0) TQSB_CASE(1) TQSB_CASE(2) TQSB_CASE(3) TQSB_CASE(4) TQSB_CASE(5)
-        TQSB_CASE(6) TQSB_CASE(7) TQSB_CASE(8) TQSB_CASE(9) TQSB_CASE(10) TQSB_CASE(11)
-        TQSB_CASE(12) TQSB_CASE(13) TQSB_CASE(14) TQSB_CASE(15) TQSB_CASE(16) TQSB_CASE(17)
-        TQSB_CASE(18) TQSB_CASE(19) TQSB_CASE(20) TQSB_CASE(21) TQSB_CASE(22) TQSB_CASE(23)
-        TQSB_CASE(24) TQSB_CASE(25) TQSB_CASE(26) TQSB_CASE(27) TQSB_CASE(28) TQSB_CASE(29)
-        TQSB_CASE(30) TQSB_CASE(31)
-#undef TQSB_CASE
-        default: break;
-    }
-    return make_float2(re, im);
-}
-
-// Scores |R'|^2 of every element go to this lane's row of the score buffer (one
-// STS.64 per slot, straight from the FFMA2 register pair) and into the lane maximum (FMNMX3;
-// NaN marks an inadmissible frequency and is ignored by max).
-template <int NS>
-__device__ __forceinline__ float score_pass(const float4 (&R)[NS], float* srow) {
-    float m4[4] = {qnan(), qnan(), qnan(), qnan()};  // 4 short FMNMX3 chains
-#pragma unroll
-    for (int i = 0; i < NS; ++i) {
-        const float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
-        const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
-        m4[i & 3] = fmax3(m4[i & 3], sc.x, sc.y);
-        st_shared_f2(srow + 2 * i, sc);
-    }
-    return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
-}
-
-// R' -= g C'[:,u] for every slot (4 FFMA2 per rank pair) from the prefetched
-// column c[], fused with the next scores.
-// PF slots of the column were issued before the pick (c[0..PF-1]); the rest stream
-// in a sliding window PF slots ahead of the update.
-template <int NS, int PF>
-__device__ __forceinline__ float update_pass(float4 (&R)[NS], float4 (&c)[NS],
-                                             const float4* __restrict__ col, int lane, float gre,
-                                             float gim, float* srow) {
-    const float2 ngre = make_float2(-gre, -gre);
-    const float2 pgim = make_float2(gim, gim);
-    const float2 ngim = make_float2(-gim, -gim);
-    float m4[4] = {qnan(), qnan(), qnan(), qnan()};  // 4 short FMNMX3 chains
-#pragma unroll
-    for (int i = 0; i < NS; ++i) {
-        if (i + PF < NS) c[i + PF] = col[(i + PF) * 32 + lane];
-        const float2 cre = make_float2(c[i].x, c[i].y), cim = make_float2(c[i].z, c[i].w);
-        float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
-        re = __ffma2_rn(ngre, cre, re);
-        re = __ffma2_rn(pgim, cim, re);
-        im = __ffma2_rn(ngre, cim, im);
-        im = __ffma2_rn(ngim, cre, im);
-        R[i] = make_float4(re.x, re.y, im.x, im.y);
-        const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
-        m4[i & 3] = fmax3(m4[i & 3], sc.x, sc.y);
-        st_shared_f2(srow + 2 * i, sc);
-    }
-    return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
-}
-
-// ---------------------------------------------------------------------------
-// Tensor memory as the hot-column tier. TMEM is 512 columns x 128 lanes x 32 bit
-// per SM and a warp reaches only its lane quadrant (lanes 32*(warp%4)..+31), so
-// each quadrant holds its own copy of the class's lowest-rank C' columns: lane j
-// of a quadrant keeps the 4*NS floats that lane j of a warp would load for that
-// column (the same float4 layout as global memory). Reads are tcgen05.ld
-// (LDTM), which bypasses the L1/shared-memory data path that the rest of the
-// loop saturates (measured on B200: ~450 B/clk/SM vs 128 for LDS.128).
-// ---------------------------------------------------------------------------
-template <int NS> struct TmemShape;  // 32x32b.x(4*NS): 4*NS consecutive columns per lane
-#define TQSB_TM_REGS16(P) P(0) P(1) P(2) P(3)
-template <int NS>
-__device__ __forceinline__ void tmem_ld(uint32_t taddr, float4 (&c)[NS]) {
-    uint32_t r[4 * NS];
-    if constexpr (NS == 16) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {"
-            "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
-            "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
-            "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-              "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]),
-              "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),
-              "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
-              "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]),
-              "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]),
-              "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
-            : "r"(taddr));
-    } else if constexpr (NS == 8) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {"
-            "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-              "=r"(r[31])
-            : "r"(taddr));
-    } else if constexpr (NS == 4) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {"
-            "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-              "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-            : "r"(taddr));
-    } else if constexpr (NS == 2) {
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                       "=r"(r[6]), "=r"(r[7])
-                     : "r"(taddr));
-    } else {
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                     : "r"(taddr));
-    }
-#pragma unroll
-    for (int i = 0; i < NS; ++i)
-        c[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                           __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-}
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// store 4 columns (one float4) per call: 32x32b.x4
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, float4 v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
-                 "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
-                 "r"(__float_as_uint(v.w))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_sync_all() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
+using namespace dev;
 
 // per-warp scratch floats: the init transpose buffer zbuf[gamma][sigma] (float2,
 // row stride 18) / half-spectrum r0buf[sigma][rho], aliased with the element-score
