@@ -101,6 +101,47 @@ __global__ void __launch_bounds__(384, 1) k_lds(float* out, int iters) {
     if (acc == 12345.f) out[threadIdx.x] = acc;
 }
 
+
+__global__ void __launch_bounds__(512, 1) k_tmem_rw(float* out, int iters) {
+    __shared__ uint32_t taddr_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&taddr_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // 16 warps: warp w owns columns 64*(w/4) .. +63 of quadrant w%4 (an R' mirror)
+    const uint32_t base = taddr_s + ((uint32_t)(32 * (warp & 3)) << 16) + 64 * (warp >> 2);
+    uint32_t x = lane;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t r[16];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(r[0]),"=r"(r[1]),"=r"(r[2]),"=r"(r[3]),"=r"(r[4]),"=r"(r[5]),"=r"(r[6]),"=r"(r[7]),
+                  "=r"(r[8]),"=r"(r[9]),"=r"(r[10]),"=r"(r[11]),"=r"(r[12]),"=r"(r[13]),"=r"(r[14]),"=r"(r[15])
+                : "r"(base + 16 * q));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] ^= x + i;
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                :: "r"(base + 16 * q), "r"(r[0]),"r"(r[1]),"r"(r[2]),"r"(r[3]),"r"(r[4]),"r"(r[5]),"r"(r[6]),"r"(r[7]),
+                  "r"(r[8]),"r"(r[9]),"r"(r[10]),"r"(r[11]),"r"(r[12]),"r"(r[13]),"r"(r[14]),"r"(r[15]));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+        x += 7;
+    }
+    if (x == 12345u) out[threadIdx.x] = x;
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr_s));
+}
+
 int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -135,5 +176,17 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     printf("smem  LDS.128     : %.3f ms  %.1f TB/s  %.1f B/clk/SM\n", ms, bytes / ms / 1e9,
            bytes / sms / (ms * 1e-3 * 1.965e9));
+    k_tmem_rw<<<sms, 512>>>(out, 100);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(a);
+    k_tmem_rw<<<sms, 512>>>(out, iters);
+    CK(cudaGetLastError());
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    cudaEventElapsedTime(&ms, a, b);
+    bytes = double(sms) * 16 * iters * 8192;  // read + write each
+    printf("tmem  R-mirror rw (4x ld.x16 + wait + st.x16, 16 warps): %.3f ms  %.1f B/clk/SM each way, %.0f cyc/warp-iter\n",
+           ms, bytes / sms / (ms * 1e-3 * 1.965e9), ms * 1e-3 * 1.965e9 / iters);
     return 0;
 }
