@@ -118,6 +118,15 @@ int tqsb_reconstruct_band(tqsb_plan* plan, const double* frame, int frame_rows, 
                           int block_row_begin, int block_row_end, double* out_band,
                           tqsb_report* rep);
 
+/* Multi-frame form (a video stream): n_frames frames of identical shape, frames[i]
+ * and outs[i] host pointers (pinned buffers are used in place; pageable ones are
+ * staged). Frames are distributed whole across the plan's devices; on each device
+ * the H2D of frame i+1 overlaps the solve of frame i and outputs are written by
+ * the kernel straight into pinned host memory. rep->blocks_processed counts all
+ * frames; rep->seconds is the device span of the batch (max over devices). */
+int tqsb_reconstruct_batch(tqsb_plan* plan, const double* const* frames, int n_frames,
+                           int frame_rows, int frame_cols, double* const* outs, tqsb_report* rep);
+
 /* Device-resident form on the plan's first device: d_frame / d_out are device
  * pointers (same layouts as tqsb_reconstruct), stream a cudaStream_t (NULL =
  * legacy default). Asynchronous: returns after enqueueing; rep->seconds is 0.

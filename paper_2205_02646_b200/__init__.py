@@ -71,6 +71,7 @@ EXPORTS = [
     "tqsb_plan_warm", "tqsb_plan_stats", "tqsb_plan_export_tables", "tqsb_plan_block_trace",
     "tqsb_generate_pattern", "tqsb_simulate", "tqsb_synthetic_image", "tqsb_psnr",
     "tqsb_host_alloc", "tqsb_host_free", "tqsb_device_count", "tqsb_probe_peaks",
+    "tqsb_reconstruct_batch",
 ]
 
 
@@ -114,6 +115,8 @@ def _load() -> C.CDLL:
     L.tqsb_host_free.argtypes = [C.c_void_p]
     L.tqsb_host_free.restype = None
     L.tqsb_probe_peaks.argtypes = [C.c_int, _dp, _dp]
+    L.tqsb_reconstruct_batch.argtypes = [C.c_void_p, C.POINTER(_dp), C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(_dp), C.POINTER(_Report)]
     return L
 
 
@@ -310,6 +313,22 @@ class Plan:
         r = _Report()
         _check(lib.tqsb_reconstruct(self._h, _d(frame), rows, cols, _d(out), refp, C.byref(r)))
         return _report(out, r)
+
+    def reconstruct_batch(self, frames: list, outs: list | None = None) -> ReconstructionReport:
+        """Frames of one shape through the pipelined multi-frame path (video stream)."""
+        frames = [np.ascontiguousarray(f, np.float64) for f in frames]
+        if not frames:
+            raise ValueError("empty batch")
+        rows, cols = frames[0].shape
+        if any(f.shape != (rows, cols) for f in frames):
+            raise ValueError("frames of a batch must share one shape")
+        if outs is None:
+            outs = [np.empty((2 * rows, 2 * cols)) for _ in frames]
+        fp = (_dp * len(frames))(*[_d(f) for f in frames])
+        op = (_dp * len(outs))(*[_d(o) for o in outs])
+        r = _Report()
+        _check(lib.tqsb_reconstruct_batch(self._h, fp, len(frames), rows, cols, op, C.byref(r)))
+        return _report(outs, r)
 
     def reconstruct_band(self, frame: np.ndarray, br0: int, br1: int,
                          out: np.ndarray | None = None) -> ReconstructionReport:

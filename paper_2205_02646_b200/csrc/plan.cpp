@@ -293,6 +293,13 @@ struct Device {
     size_t h_in_cap = 0;
     double* h_out = nullptr;
     size_t h_out_cap = 0;
+    // multi-frame pipeline (tqsb_reconstruct_batch): double-buffered frames/staging
+    double* d_fs[2] = {};
+    size_t fs_cap[2] = {};
+    double* h_in_s[2] = {};
+    size_t h_in_s_cap[2] = {};
+    double* h_out_s[2] = {};
+    size_t h_out_s_cap[2] = {};
     size_t table_bytes = 0;
 };
 
@@ -357,6 +364,11 @@ void device_free(Device* d) {
     cudaFree(d->d_out);
     if (d->h_in) cudaFreeHost(d->h_in);
     if (d->h_out) cudaFreeHost(d->h_out);
+    for (int k = 0; k < 2; ++k) {
+        cudaFree(d->d_fs[k]);
+        if (d->h_in_s[k]) cudaFreeHost(d->h_in_s[k]);
+        if (d->h_out_s[k]) cudaFreeHost(d->h_out_s[k]);
+    }
     if (d->ev0) cudaEventDestroy(d->ev0);
     if (d->ev1) cudaEventDestroy(d->ev1);
     for (int k = 0; k < 4; ++k) {
@@ -673,6 +685,89 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
     if (!out_pinned) par_memcpy(out_band, d->h_out, sizeof(double) * out_n);
 }
 
+// Multi-frame pipeline on one device: frame i+1's H2D (copy stream) overlaps frame
+// i's solve; outputs are stored zero-copy into pinned host memory by the kernel.
+// Pageable frames/outputs go through double-buffered pinned staging.
+void run_batch_host(tqsb_plan* p, Device* d, const Geometry& g, const double* const* frames,
+                    int frame_rows, int frame_cols, double* const* outs, int n, BandResult* r) {
+    auto fail = [&](int rc) {
+        r->rc = rc;
+        r->err = g_error;
+    };
+    if (n <= 0) return;
+    if (cudaSetDevice(d->id) != cudaSuccess) return fail(set_error(TQSB_ECUDA, "cudaSetDevice"));
+    Work* w = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int nbr = g.padM / g.B;
+    int rc = prepare_band(p, d, g, frame_rows, frame_cols, 0, nbr, &w, &r->created, &r->launches);
+    if (rc) return fail(rc);
+    r->warm = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r->classes_total = w->classes_total;
+    r->classes_interior = w->classes_interior;
+    r->blocks = (long long)w->n_tasks * n;
+    const size_t in_n = size_t(frame_rows) * frame_cols;
+    const size_t out_n = size_t(g.M) * g.N;
+    for (int k = 0; k < 2; ++k) {
+        if ((rc = ensure_buffer(&d->d_fs[k], &d->fs_cap[k], in_n))) return fail(rc);
+        if ((rc = ensure_pinned(&d->h_in_s[k], &d->h_in_s_cap[k], in_n))) return fail(rc);
+        if ((rc = ensure_pinned(&d->h_out_s[k], &d->h_out_s_cap[k], out_n))) return fail(rc);
+    }
+    std::vector<char> out_pinned(n);
+    for (int i = 0; i < n; ++i) out_pinned[i] = is_pinned(outs[i]);
+    for (int i = 0; i < n; ++i) {
+        const int s = i & 1;
+        const double* src = frames[i];
+        if (!is_pinned(src)) {
+            if (i >= 2) cudaEventSynchronize(d->ev_h2d[s]);  // staging slot free again
+            par_memcpy(d->h_in_s[s], src, sizeof(double) * in_n);
+            src = d->h_in_s[s];
+        }
+        if (i >= 2) cudaStreamWaitEvent(d->s_h2d, d->ev_comp[s], 0);  // frame i-2 done with d_fs[s]
+        cudaMemcpyAsync(d->d_fs[s], src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->s_h2d);
+        cudaEventRecord(d->ev_h2d[s], d->s_h2d);
+        cudaStreamWaitEvent(d->stream, d->ev_h2d[s], 0);
+        double* host_out = outs[i];
+        if (!out_pinned[i]) {
+            if (i >= 2) {  // frame i-2's kernel wrote h_out_s[s]; hand it over first
+                cudaEventSynchronize(d->ev_comp[s]);
+                if (!out_pinned[i - 2]) par_memcpy(outs[i - 2], d->h_out_s[s], sizeof(double) * out_n);
+            }
+            host_out = d->h_out_s[s];
+        }
+        double* dev_view = nullptr;
+        if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_view), host_out, 0) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(set_error(TQSB_ECUDA, "output buffer is not device-mapped pinned memory"));
+        }
+        SolveArgs a = base_args(p, d);
+        a.frame = d->d_fs[s];
+        a.frame_rows = frame_rows;
+        a.frame_cols = frame_cols;
+        a.frame_row0 = 0;
+        a.frame_pitch = frame_cols;
+        a.out = dev_view;
+        a.out_row0 = 0;
+        a.out_rows = g.M;
+        a.out_cols = g.N;
+        a.tasks = w->d_tasks;
+        a.items = w->d_items;
+        a.n_items = w->n_items;
+        if (i == 0) cudaEventRecord(d->ev0, d->stream);
+        if (w->n_items > 0) {
+            if ((rc = launch(p, d, a, d->stream))) return fail(rc);
+            r->launches += 1;
+        }
+        cudaEventRecord(d->ev_comp[s], d->stream);
+    }
+    cudaEventRecord(d->ev1, d->stream);
+    cudaError_t e = cudaStreamSynchronize(d->stream);
+    if (e != cudaSuccess)
+        return fail(set_error(TQSB_ECUDA, std::string("solve: ") + cudaGetErrorString(e)));
+    for (int i = std::max(0, n - 2); i < n; ++i)
+        if (!out_pinned[i]) par_memcpy(outs[i], d->h_out_s[i & 1], sizeof(double) * out_n);
+    cudaEventElapsedTime(&r->ms, d->ev0, d->ev1);
+}
+
 void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const Geometry& g,
                  long long classes_total, long long classes_interior, double e2e) {
     if (!rep) return;
@@ -892,6 +987,37 @@ int tqsb_reconstruct(tqsb_plan* p, const double* frame, int frame_rows, int fram
             rep->has_psnr = 1;
         }
     }
+    return TQSB_OK;
+}
+
+int tqsb_reconstruct_batch(tqsb_plan* p, const double* const* frames, int n_frames,
+                           int frame_rows, int frame_cols, double* const* outs, tqsb_report* rep) {
+    if (!p || !frames || !outs || n_frames < 0) return set_error(TQSB_EINVAL, "null argument");
+    for (int i = 0; i < n_frames; ++i)
+        if (!frames[i] || !outs[i]) return set_error(TQSB_EINVAL, "null frame or output pointer");
+    std::lock_guard<std::mutex> lk(p->mu);
+    const auto t0 = std::chrono::steady_clock::now();
+    Geometry g;
+    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    const int nd = std::max(1, std::min<int>(int(p->devs.size()), n_frames));
+    std::vector<BandResult> rs(nd);
+    std::vector<int> cut(nd + 1);
+    for (int i = 0; i <= nd; ++i) cut[i] = int((long long)n_frames * i / nd);
+    if (nd == 1) {
+        run_batch_host(p, p->devs[0].get(), g, frames, frame_rows, frame_cols, outs, n_frames, &rs[0]);
+    } else {  // whole frames per device, one host thread each
+        std::vector<std::thread> th;
+        for (int i = 0; i < nd; ++i)
+            th.emplace_back([&, i] {
+                run_batch_host(p, p->devs[i].get(), g, frames + cut[i], frame_rows, frame_cols,
+                               outs + cut[i], cut[i + 1] - cut[i], &rs[i]);
+            });
+        for (auto& t : th) t.join();
+    }
+    for (auto& r : rs)
+        if (r.rc) return set_error(r.rc, r.err);
+    const double e2e = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    fill_report(rep, rs, g, rs[0].classes_total, rs[0].classes_interior, e2e);
     return TQSB_OK;
 }
 

@@ -280,3 +280,29 @@ def test_validation_through_plan(tq, need_gpu):
         tq.reconstruct(np.zeros((0, 0)), pat, tq.ReconstructionConfig())
     with pytest.raises(ValueError, match="above 32"):
         tq.Plan(pat, tq.ReconstructionConfig(window=64))
+
+
+def test_batch_matches_single_frames(tq, need_gpu):
+    """tqsb_reconstruct_batch (video path): bitwise equal to per-frame calls, for
+    pageable and pinned host buffers, odd batch sizes included."""
+    import ctypes
+    pat = tq.generate_pattern(7, 16)
+    cfg = tq.ReconstructionConfig(max_iterations=60)
+    frames = [tq.simulate_measurement(tq.synthetic_image(96, 128, 1000 + i), pat) for i in range(5)]
+    with tq.Plan(pat, cfg) as plan:
+        singles = [plan.reconstruct(f).output.copy() for f in frames]
+        rep = plan.reconstruct_batch(frames)
+        for o, want in zip(rep.output, singles):
+            np.testing.assert_array_equal(o, want)
+        assert rep.blocks_processed == 5 * (96 // 4) * (128 // 4) and rep.gpu_launches == 5
+        # pinned outputs: written in place by the kernel (zero-copy)
+        ptrs = [tq.lib.tqsb_host_alloc(96 * 128 * 8) for _ in frames]
+        try:
+            outs = [np.ctypeslib.as_array((ctypes.c_double * (96 * 128)).from_address(p)).reshape(96, 128)
+                    for p in ptrs]
+            plan.reconstruct_batch(frames, outs)
+            for o, want in zip(outs, singles):
+                np.testing.assert_array_equal(o, want)
+        finally:
+            for p in ptrs:
+                tq.lib.tqsb_host_free(p)
