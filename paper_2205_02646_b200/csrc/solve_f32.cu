@@ -30,6 +30,13 @@
 #include "tqsb_internal.hpp"
 #include "solve_common.cuh"
 
+#ifndef TQSB_KEYS
+#define TQSB_KEYS 0
+#endif
+#ifndef TQSB_BRX
+#define TQSB_BRX 0
+#endif
+
 namespace tqsb {
 namespace {
 
@@ -46,7 +53,7 @@ struct Scratch {
     static constexpr int kFloats = (kZ > kR ? (kZ > kS ? kZ : kS) : (kR > kS ? kR : kS));
 };
 
-template <int NS, int W, int PPL>
+template <int NS, int W, int PPL, bool TRACE>
 __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs a) {
     extern __shared__ __align__(16) float smem[];
     constexpr int COLF4 = NS * 32;  // float4 per column
@@ -183,7 +190,11 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 R[i] = make_float4(re.x, re.y, im.x, im.y);
             }
             __syncwarp();
+#if TQSB_KEYS
+            float lmax = score_pass_keys<NS>(R);
+#else
             float lmax = score_pass<NS>(R, srow);
+#endif
 
             float acc[PPL];
 #pragma unroll
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 pe[j] = unsigned(rw + (p_r[j] < 0 ? 0 : p_r[j]));
                 pg[j] = unsigned(cw + p_c[j]);
             }
-            const bool tracing = a.trace_picks != nullptr && ti == 0;
+            const bool tracing = TRACE && ti == 0;
 
             int it = 0;
             for (; it < a.iterations; ++it) {
@@ -204,6 +215,10 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 // ---- argmax over the warp (NaN = inadmissible, ignored by max) ----
                 const float gmax = warp_max_f32(lmax);
                 if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
+#if TQSB_KEYS
+                const int t = 31 - int(__float_as_uint(gmax) & 31u);
+                const int Lw = __ffs(__ballot_sync(FULL, lmax == gmax)) - 1;
+#else
                 const unsigned cand = __ballot_sync(FULL, lmax == gmax);
                 int Lw = __ffs(cand) - 1;
                 const float sv = lane < 2 * NS ? scr[Lw * kSbufStride + lane] : qnan();
@@ -228,6 +243,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                     Lw = (r >> 1) & 31;
                     t = 2 * (r >> 6) + (r & 1);
                 }
+#endif
                 const int slot = t >> 1, b = t & 1;
                 const int u = 64 * slot + 2 * Lw + b;
                 // ---- issue the whole C' column now; its latency overlaps the pick ----
@@ -241,30 +257,43 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 #pragma unroll
                     for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
                 }
-                const float2 v = pick_elem<NS>(R, t);
+                const int2 meta = s_meta[u];  // (fac bits, flat k) of rank u
+                float2 v;
+                if constexpr (NS == 16 && TQSB_BRX)
+                    v = pick_elem_brx(R, t);
+                else
+                    v = pick_elem<NS>(R, t);
                 const float ure = __shfl_sync(FULL, v.x, Lw);
                 const float uim = __shfl_sync(FULL, v.y, Lw);
-                const int2 meta = s_meta[u];  // (fac bits, flat k) of rank u
                 const float f = __int_as_float(meta.x);
                 const float gre = f * ure, gim = f * uim;
                 const int kflat = meta.y;
+                // synthesis phases of the kept pixels: issued now, consumed after the update
+                const unsigned sigma = unsigned(kflat) / W, rho = unsigned(kflat) % W;
+                float2 ph[PPL];
+#pragma unroll
+                for (int j = 0; j < PPL; ++j) ph[j] = unit[(pe[j] * sigma + pg[j] * rho) % unsigned(W)];
+#if !TQSB_KEYS
                 __syncwarp();  // all score reads of this iteration precede the rewrite
+#endif
+#if TQSB_KEYS
+                if (in_tmem) {
+                    tmem_wait_ld();
+                    lmax = update_pass_keys<NS, NS>(R, c, col, lane, gre, gim);
+                } else {
+                    lmax = update_pass_keys<NS, PF>(R, c, col, lane, gre, gim);
+                }
+#else
                 if (in_tmem) {
                     tmem_wait_ld();
                     lmax = update_pass<NS, NS>(R, c, col, lane, gre, gim, srow);
                 } else {
                     lmax = update_pass<NS, PF>(R, c, col, lane, gre, gim, srow);
                 }
+#endif
                 // ---- synthesis of the kept block pixels (off the critical path) ----
-                const unsigned sigma = unsigned(kflat) / W, rho = unsigned(kflat) % W;
 #pragma unroll
-                for (int j = 0; j < PPL; ++j) {
-                    if (p_r[j] >= 0) {
-                        const unsigned idx = (pe[j] * sigma + pg[j] * rho) % unsigned(W);
-                        const float2 ph = unit[idx];
-                        acc[j] = fmaf(gre, ph.x, fmaf(-gim, ph.y, acc[j]));
-                    }
-                }
+                for (int j = 0; j < PPL; ++j) acc[j] = fmaf(gre, ph[j].x, fmaf(-gim, ph[j].y, acc[j]));
                 if (tracing && lane == 0) {
                     a.trace_picks[it] = kflat;
                     a.trace_gd[2 * it] = gre;
@@ -310,7 +339,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 template <int NS, int W, int PPL>
 int launch_one(const SolveArgs& a, cudaStream_t stream, int num_sms) {
     const size_t smem = solve_f32_smem_bytes(NS, a.hot) ;
-    auto kern = k_solve_f32<NS, W, PPL>;
+    auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true> : k_solve_f32<NS, W, PPL, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
@@ -353,6 +382,10 @@ int solve_f32_max_hot(int n_slots, int device) {
 
 int launch_solve_f32(const SolveArgs& a, int n_slots, void* stream, int num_sms) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+#ifdef TQSB_ONLY_W32  // experiment builds (tools/variants.py): the default window only
+    if (a.window == 32) return launch_w<32>(a, n_slots, s, num_sms);
+    return cudaErrorInvalidValue;
+#endif
     switch (a.window) {
         case 2: return launch_w<2>(a, n_slots, s, num_sms);
         case 4: return launch_w<4>(a, n_slots, s, num_sms);
