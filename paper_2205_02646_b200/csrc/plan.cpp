@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <tuple>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -216,20 +217,29 @@ WindowTables window_tables(const tqsb_config& c) {
     for (int i = 0; i < 2 * W; ++i) t.unit32[i] = float(t.unit64[i]);
     t.q.resize(t.K);
     const int half = W / 2;
-    std::vector<std::pair<int, int>> order;
+    // Rank order: by centred radius (hot first), conjugate pairs k / -k on adjacent
+    // ranks 2j (smaller flat k) and 2j+1, i.e. the two halves of one lane's slot, so
+    // the packed selection key resolves their bitwise ties to the smaller flat k like
+    // the reference's strict '>' scan (rljsde.cpp:147-156). The four self-conjugate
+    // frequencies pair among themselves: DC with (W/2, W/2) on ranks 0/1, (0, W/2)
+    // with (W/2, 0) at their radius.
+    std::vector<std::tuple<int, int, int>> order;  // (group radius^2, pair id, k)
     for (int s = 0; s < W; ++s)
         for (int r = 0; r < W; ++r) {  // frequency_weight (basis.cpp:90-97)
             const int cs = s <= half ? s : W - s, cr = r <= half ? r : W - r;
             const double radius = std::sqrt(double(cs) * cs + double(cr) * cr);
             const double maxr = 1.41421356237309504880 * half * (1.0 + 1e-6);
             t.q[s * W + r] = std::pow(1.0 - radius / maxr, c.frequency_exponent);
-            order.emplace_back(cs * cs + cr * cr, s * W + r);
+            const int k = s * W + r, kc = ((W - s) % W) * W + (W - r) % W;
+            int grp = cs * cs + cr * cr, pid = std::min(k, kc);
+            if (k == kc && cs == half && cr == half) grp = 0, pid = 0;  // (W/2, W/2) next to DC
+            order.emplace_back(grp, pid, k);
         }
     std::sort(order.begin(), order.end());
     t.perm.assign(t.K_pad, -1);
     t.src.assign(t.K_pad, 0);
     for (int r = 0; r < t.K; ++r) {
-        const int k = order[r].second, s = k / W, rho = k % W;
+        const int k = std::get<2>(order[r]), s = k / W, rho = k % W;
         t.perm[r] = k;
         // half-spectrum source: rows sigma <= W/2, with the self-conjugate rows
         // 0 and W/2 taking rho > W/2 from their mirror

@@ -134,18 +134,28 @@ __device__ __forceinline__ float score_pass(const float4 (&R)[NS], float* srow) 
 // position t = 2*slot + half stored as 31 - t in the low 5 mantissa bits, so one
 // FMNMX3/CREDUX max yields both the maximum and (with a lane ballot) its position.
 // Scores that differ by less than 2^-18 relative compare by position instead.
-__device__ __forceinline__ float score_key(float s, int t) {
-    return __uint_as_float((__float_as_uint(s) & 0xffffffe0u) | unsigned(31 - t));
+// one LOP3 per element: (bits & mask) | (31 - t) with the mask held in a register
+// (keymask(), opaque to constant folding) and 31 - t as the instruction immediate
+__device__ __forceinline__ unsigned keymask() {
+    unsigned m;
+    asm volatile("mov.b32 %0, 0xffffffe0;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ float score_key(float s, int t, unsigned mask) {
+    unsigned d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(d) : "r"(__float_as_uint(s)), "r"(unsigned(31 - t)), "r"(mask));
+    return __uint_as_float(d);
 }
 
 template <int NS>
 __device__ __forceinline__ float score_pass_keys(const float4 (&R)[NS]) {
     float m4[4] = {qnan(), qnan(), qnan(), qnan()};
+    const unsigned kmask = keymask();
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         const float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
         const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
-        m4[i & 3] = fmax3(m4[i & 3], score_key(sc.x, 2 * i), score_key(sc.y, 2 * i + 1));
+        m4[i & 3] = fmax3(m4[i & 3], score_key(sc.x, 2 * i, kmask), score_key(sc.y, 2 * i + 1, kmask));
     }
     return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
 }
@@ -158,6 +168,7 @@ __device__ __forceinline__ float update_pass_keys(float4 (&R)[NS], float4 (&c)[N
     const float2 pgim = make_float2(gim, gim);
     const float2 ngim = make_float2(-gim, -gim);
     float m4[4] = {qnan(), qnan(), qnan(), qnan()};
+    const unsigned kmask = keymask();
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         if (i + PF < NS) c[i + PF] = col[(i + PF) * 32 + lane];
@@ -169,7 +180,7 @@ __device__ __forceinline__ float update_pass_keys(float4 (&R)[NS], float4 (&c)[N
         im = __ffma2_rn(ngim, cre, im);
         R[i] = make_float4(re.x, re.y, im.x, im.y);
         const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
-        m4[i & 3] = fmax3(m4[i & 3], score_key(sc.x, 2 * i), score_key(sc.y, 2 * i + 1));
+        m4[i & 3] = fmax3(m4[i & 3], score_key(sc.x, 2 * i, kmask), score_key(sc.y, 2 * i + 1, kmask));
     }
     return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
 }
@@ -270,6 +281,114 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float4 (&c)[NS]) {
     for (int i = 0; i < NS; ++i)
         c[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                            __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+}
+
+// Windowed column stream for NS == 16 (register budget: at most 12 column slots
+// live). Slots [0, PF) were issued before the pick into c[]; global slots stream
+// PF ahead of the update; TMEM slots arrive in 4-slot (x16) chunks, each issued
+// one chunk after the previous wait::ld so that a wait never covers a fresh load.
+template <int NS, int PF, bool TM, bool KEYS>
+__device__ __forceinline__ float update_win(float4 (&R)[NS], float4 (&c)[NS],
+                                            const float4* __restrict__ col, uint32_t taddr,
+                                            int lane, float gre, float gim, float* srow) {
+    const float2 ngre = make_float2(-gre, -gre);
+    const float2 pgim = make_float2(gim, gim);
+    const float2 ngim = make_float2(-gim, -gim);
+    float m4[4] = {qnan(), qnan(), qnan(), qnan()};
+    const unsigned kmask = keymask();
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        if constexpr (TM) {
+            if (i % 4 == 0) {
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (i + PF < NS) {
+                    float4 t4[4];
+                    tmem_ld<4>(taddr + uint32_t(4 * (i + PF)), t4);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) c[i + PF + k] = t4[k];
+                }
+            }
+        } else {
+            if (i + PF < NS) c[i + PF] = __ldg(col + (i + PF) * 32 + lane);
+        }
+        const float2 cre = make_float2(c[i].x, c[i].y), cim = make_float2(c[i].z, c[i].w);
+        float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
+        re = __ffma2_rn(ngre, cre, re);
+        re = __ffma2_rn(pgim, cim, re);
+        im = __ffma2_rn(ngre, cim, im);
+        im = __ffma2_rn(ngim, cre, im);
+        R[i] = make_float4(re.x, re.y, im.x, im.y);
+        const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
+        if constexpr (KEYS) {
+            m4[i & 3] = fmax3(m4[i & 3], score_key(sc.x, 2 * i, kmask), score_key(sc.y, 2 * i + 1, kmask));
+        } else {
+            m4[i & 3] = fmax3(m4[i & 3], sc.x, sc.y);
+            st_shared_f2(srow + 2 * i, sc);
+        }
+    }
+    return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
+}
+
+// Four column slots (16 floats per lane) into d[] from TMEM (tm) or global memory
+// (g = column + slot0 * 32 + lane): one code path for both tiers, so the residual
+// registers keep a single allocation. The tcgen05.ld is predicated on a warp-uniform
+// flag; a following tcgen05.wait::ld (unconditional) completes it.
+__device__ __forceinline__ void load_chunk(bool tm, uint32_t taddr, const float4* g, float4 (&d)[4]) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %18, 0;\n\t"
+        "@p tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+        "@!p ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%17];\n\t"
+        "@!p ld.global.nc.v4.f32 {%4,%5,%6,%7}, [%17+512];\n\t"
+        "@!p ld.global.nc.v4.f32 {%8,%9,%10,%11}, [%17+1024];\n\t"
+        "@!p ld.global.nc.v4.f32 {%12,%13,%14,%15}, [%17+1536];\n\t}"
+        : "=f"(d[0].x), "=f"(d[0].y), "=f"(d[0].z), "=f"(d[0].w), "=f"(d[1].x), "=f"(d[1].y),
+          "=f"(d[1].z), "=f"(d[1].w), "=f"(d[2].x), "=f"(d[2].y), "=f"(d[2].z), "=f"(d[2].w),
+          "=f"(d[3].x), "=f"(d[3].y), "=f"(d[3].z), "=f"(d[3].w)
+        : "r"(taddr), "l"(g), "r"(int(tm))
+        : "memory");
+}
+
+// One update path for both tiers (NS == 16): chunks 0 and 1 (slots 0-7) were issued
+// before the pick; chunk k+2 is issued at the start of chunk k, after the wait::ld
+// that completes chunk k+1.
+template <int NS, bool KEYS, int AHEAD>
+__device__ __forceinline__ float update_uni(float4 (&R)[NS], float4 (&c)[NS], bool tm,
+                                            uint32_t taddr, const float4* __restrict__ gl,
+                                            float gre, float gim, float* srow) {
+    static_assert(NS == 16, "update_uni streams four 4-slot chunks");
+    const float2 ngre = make_float2(-gre, -gre);
+    const float2 pgim = make_float2(gim, gim);
+    const float2 ngim = make_float2(-gim, -gim);
+    float m4[4] = {qnan(), qnan(), qnan(), qnan()};
+    [[maybe_unused]] const unsigned kmask = keymask();
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        if (i % 4 == 0) {
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            constexpr int A = 4 * AHEAD;  // slots issued ahead of the update
+            if (i + A < NS) {
+                float4 t4[4];
+                load_chunk(tm, taddr + uint32_t(4 * (i + A)), gl + (i + A) * 32, t4);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c[i + A + k] = t4[k];
+            }
+        }
+        const float2 cre = make_float2(c[i].x, c[i].y), cim = make_float2(c[i].z, c[i].w);
+        float2 re = make_float2(R[i].x, R[i].y), im = make_float2(R[i].z, R[i].w);
+        re = __ffma2_rn(ngre, cre, re);
+        re = __ffma2_rn(pgim, cim, re);
+        im = __ffma2_rn(ngre, cim, im);
+        im = __ffma2_rn(ngim, cre, im);
+        R[i] = make_float4(re.x, re.y, im.x, im.y);
+        const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
+        if constexpr (KEYS) {
+            m4[i & 3] = fmax3(m4[i & 3], score_key(sc.x, 2 * i, kmask), score_key(sc.y, 2 * i + 1, kmask));
+        } else {
+            m4[i & 3] = fmax3(m4[i & 3], sc.x, sc.y);
+            st_shared_f2(srow + 2 * i, sc);
+        }
+    }
+    return fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan());
 }
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }

@@ -31,10 +31,19 @@
 #include "solve_common.cuh"
 
 #ifndef TQSB_KEYS
-#define TQSB_KEYS 0
+#define TQSB_KEYS 1  // packed score/position keys (see score_key)
 #endif
 #ifndef TQSB_BRX
 #define TQSB_BRX 0
+#endif
+#ifndef TQSB_WIN
+#define TQSB_WIN 0
+#endif
+#ifndef TQSB_UNI
+#define TQSB_UNI 1
+#endif
+#ifndef TQSB_AHEAD
+#define TQSB_AHEAD 2  // 4-slot chunks in flight ahead of the update (TQSB_UNI)
 #endif
 
 namespace tqsb {
@@ -216,7 +225,9 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 const float gmax = warp_max_f32(lmax);
                 if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
 #if TQSB_KEYS
-                const int t = 31 - int(__float_as_uint(gmax) & 31u);
+                // t through a vector register (a uniform-register switch makes ptxas spill R)
+                int t;
+                asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(31 - int(__float_as_uint(gmax) & 31u)));
                 const int Lw = __ffs(__ballot_sync(FULL, lmax == gmax)) - 1;
 #else
                 const unsigned cand = __ballot_sync(FULL, lmax == gmax);
@@ -247,12 +258,36 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 const int slot = t >> 1, b = t & 1;
                 const int u = 64 * slot + 2 * Lw + b;
                 // ---- issue the whole C' column now; its latency overlaps the pick ----
-                constexpr int PF = NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH;
+                // windowed column stream (NS == 16, TQSB_WIN): 8 slots ahead
+                constexpr bool kWin = NS == 16 && TQSB_WIN;
+                constexpr bool kUni = NS == 16 && TQSB_UNI;  // one update path for both tiers
+                constexpr int PF = (kWin || kUni) ? 8 : (NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH);
                 float4 c[NS];
                 const float4* col = gcols + size_t(u) * COLF4;
                 const bool in_tmem = u < hotn;
-                if (in_tmem) {
-                    tmem_ld<NS>(tq + uint32_t(u * 4 * NS), c);
+                const uint32_t tcol = tq + uint32_t(u * 4 * NS);
+                if constexpr (kUni) {
+                    float4 t4[4];
+                    load_chunk(in_tmem, tcol, col + lane, t4);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) c[k] = t4[k];
+                    if constexpr (TQSB_AHEAD > 1) {
+                        load_chunk(in_tmem, tcol + 16u, col + 4 * 32 + lane, t4);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) c[4 + k] = t4[k];
+                    }
+                } else if constexpr (kWin) {
+                    if (in_tmem) {
+                        float4 t8[PF];
+                        tmem_ld<PF>(tcol, t8);
+#pragma unroll
+                        for (int i = 0; i < PF; ++i) c[i] = t8[i];
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
+                    }
+                } else if (in_tmem) {
+                    tmem_ld<NS>(tcol, c);
                 } else {
 #pragma unroll
                     for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
@@ -276,6 +311,14 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 #if !TQSB_KEYS
                 __syncwarp();  // all score reads of this iteration precede the rewrite
 #endif
+                if constexpr (kUni) {
+                    lmax = update_uni<NS, TQSB_KEYS, TQSB_AHEAD>(R, c, in_tmem, tcol, col + lane, gre, gim, srow);
+                } else if constexpr (kWin) {
+                    if (in_tmem)
+                        lmax = update_win<NS, PF, true, TQSB_KEYS>(R, c, col, tcol, lane, gre, gim, srow);
+                    else
+                        lmax = update_win<NS, PF, false, TQSB_KEYS>(R, c, col, tcol, lane, gre, gim, srow);
+                } else {
 #if TQSB_KEYS
                 if (in_tmem) {
                     tmem_wait_ld();
@@ -291,6 +334,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                     lmax = update_pass<NS, PF>(R, c, col, lane, gre, gim, srow);
                 }
 #endif
+                }
                 // ---- synthesis of the kept block pixels (off the critical path) ----
 #pragma unroll
                 for (int j = 0; j < PPL; ++j) acc[j] = fmaf(gre, ph[j].x, fmaf(-gim, ph[j].y, acc[j]));
