@@ -13,7 +13,7 @@
  * reference's exception types in include/tqsb/reconstruct.hpp:
  *   TQSB_EINVAL -> std::invalid_argument   (pipeline.cpp:27-42, 66-67, 74-75, 180-181)
  *   TQSB_ELOGIC -> std::logic_error         (pipeline.cpp:146-147)
- *   TQSB_ECUDA / TQSB_ENOMEM / TQSB_ENODEV -> std::runtime_error
+ *   TQSB_ECUDA / TQSB_ENOMEM / TQSB_ENODEV / TQSB_EIO -> std::runtime_error
  * The message of the last failure on the calling thread is tqsb_last_error().
  */
 #ifndef TQSB_H
@@ -32,6 +32,7 @@ extern "C" {
 #define TQSB_ENOMEM 3
 #define TQSB_ELOGIC 4
 #define TQSB_ENODEV 5
+#define TQSB_EIO 6     /* file format / I/O failure -> std::runtime_error ("<path>: <what>") */
 
 /* Reference Precision (rljsde.hpp:22): storage precision of the reference's tables. */
 #define TQSB_PRECISION_SINGLE 0
@@ -175,6 +176,28 @@ int tqsb_simulate(const double* image, int rows, int cols, const uint8_t* opaque
 int tqsb_synthetic_image(int rows, int cols, uint64_t seed, double* out);
 /* psnr (pipeline.cpp:221-233): +inf when identical. */
 double tqsb_psnr(const double* reference, const double* estimate, long long n);
+
+/* File formats (include/tqs/io.hpp:1-35, src/io.cpp of the reference); byte-identical
+ * output, the same acceptance rules and "<path>: <what>" messages. No device needed.
+ * tqsb_io_read: kind TQSB_IO_PGM (P5, 8/16-bit, samples / maxval), TQSB_IO_TQSM
+ * (frame or raw image dump) or TQSB_IO_ANY (sniffs "TQSM", else PGM: read_image_any).
+ * Pass out = NULL to query rows/cols; out receives rows*cols float64 row-major. */
+#define TQSB_IO_ANY 0
+#define TQSB_IO_PGM 1
+#define TQSB_IO_TQSM 2
+int tqsb_io_read(const char* path, int kind, int* rows, int* cols, double* out);
+/* write_pgm (io.cpp:99-131): bits 8 or 16, values clamped to [0,1] and rounded. */
+int tqsb_io_write_pgm(const char* path, const double* image, int rows, int cols, int bits);
+/* TQSM container: "TQSM", u32 rows, u32 cols (LE), float64 payload (write_frame /
+ * write_raw_image). */
+int tqsb_io_write_tqsm(const char* path, const double* values, int rows, int cols);
+/* TQSP pattern text (read_pattern / write_pattern, io.cpp:133-199). rng receives the
+ * generator name (NUL-terminated, truncated to rng_cap-1); opaque (nullable) receives
+ * (period/2)^2 quadrant indices. */
+int tqsb_io_read_pattern(const char* path, int* period, uint64_t* seed, char* rng, size_t rng_cap,
+                         uint8_t* opaque);
+int tqsb_io_write_pattern(const char* path, int period, uint64_t seed, const char* rng,
+                          const uint8_t* opaque);
 
 /* Pinned host memory for zero-staging transfers (cudaHostAlloc). */
 void* tqsb_host_alloc(size_t bytes);

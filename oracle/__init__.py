@@ -192,7 +192,105 @@ class Reference:
                                      C.c_double, C.c_int, _ip, _dp, _dp, _dp, _dp, _dp, _dp]
         L.ref_block_trace.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int,
                                       C.c_double, C.c_double, C.c_double, C.c_int, _ip, _dp, _dp]
+        L.ref_io_write_pgm.argtypes = [C.c_char_p, _dp, C.c_int, C.c_int, C.c_int]
+        L.ref_io_read.argtypes = [C.c_char_p, C.c_int, _ip, _ip, _dp]
+        L.ref_io_write_tqsm.argtypes = [C.c_char_p, _dp, C.c_int, C.c_int]
+        L.ref_io_write_pattern.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_char_p, _u8p]
+        L.ref_io_read_pattern.argtypes = [C.c_char_p, _ip, C.POINTER(C.c_uint64), C.c_char_p,
+                                          C.c_size_t, _u8p]
+        L.ref_pattern_digest.argtypes = [_u8p, C.c_int]
+        L.ref_pattern_digest.restype = C.c_uint64
+        L.ref_save_cache.argtypes = [C.c_void_p, C.c_char_p, _u8p, C.c_int, C.c_int, C.c_int,
+                                     C.c_double, C.c_double]
+        L.ref_load_cache.argtypes = L.ref_save_cache.argtypes
+        L.ref_memory_report.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_uint64)]
+        L.ref_reconstruct_algo.argtypes = [_dp, C.c_int, C.c_int, _u8p, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _dp,
+                                           _dp]
+        L.ref_ljsde_trace.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int,
+                                      C.c_double, _ip, _dp, _dp]
         self.lib = L
+
+    # ---- file formats (tqs::read_* / write_*, io.cpp)
+    def write_pgm(self, path, img, bits=8):
+        img = np.ascontiguousarray(img, np.float64)
+        rows, cols = img.shape if img.ndim == 2 else (0, 0)
+        self._check(self.lib.ref_io_write_pgm(os.fsencode(path), _d(img) if img.size else None,
+                                              rows, cols, bits))
+
+    def read(self, path, kind=0):
+        r, c = C.c_int(), C.c_int()
+        self._check(self.lib.ref_io_read(os.fsencode(path), kind, C.byref(r), C.byref(c), None))
+        out = np.zeros((r.value, c.value))
+        self._check(self.lib.ref_io_read(os.fsencode(path), kind, C.byref(r), C.byref(c),
+                                         _d(out)))
+        return out
+
+    def write_tqsm(self, path, v):
+        v = np.ascontiguousarray(v, np.float64)
+        self._check(self.lib.ref_io_write_tqsm(os.fsencode(path), _d(v), v.shape[0], v.shape[1]))
+
+    def write_pattern(self, path, period, seed, rng, opaque):
+        opaque = np.ascontiguousarray(opaque, np.uint8)
+        self._check(self.lib.ref_io_write_pattern(os.fsencode(path), period, seed, rng.encode(),
+                                                  opaque.ctypes.data_as(_u8p)))
+
+    def read_pattern(self, path):
+        per, seed = C.c_int(), C.c_uint64()
+        rng = C.create_string_buffer(256)
+        self._check(self.lib.ref_io_read_pattern(os.fsencode(path), C.byref(per), C.byref(seed),
+                                                 rng, 256, None))
+        opq = np.zeros((per.value // 2) ** 2, np.uint8)
+        self._check(self.lib.ref_io_read_pattern(os.fsencode(path), C.byref(per), C.byref(seed),
+                                                 rng, 256, opq.ctypes.data_as(_u8p)))
+        return per.value, seed.value, rng.value.decode(), opq
+
+    # ---- TQSK persistence / accounting
+    def pattern_digest(self, opaque, period):
+        return self.lib.ref_pattern_digest(np.ascontiguousarray(opaque, np.uint8).ctypes.data_as(_u8p),
+                                           period)
+
+    def save_cache(self, cache, path, opaque, period, window, double=True, decay=0.8,
+                   exponent=2.0):
+        self._check(self.lib.ref_save_cache(cache, os.fsencode(path),
+                                            np.ascontiguousarray(opaque, np.uint8).ctypes.data_as(_u8p),
+                                            period, window, int(double), decay, exponent))
+
+    def load_cache(self, cache, path, opaque, period, window, double=True, decay=0.8,
+                   exponent=2.0):
+        return self._check(self.lib.ref_load_cache(
+            cache, os.fsencode(path), np.ascontiguousarray(opaque, np.uint8).ctypes.data_as(_u8p),
+            period, window, int(double), decay, exponent))
+
+    def memory_report(self, classes, window, double, local=-1):
+        out = (C.c_uint64 * 4)()
+        self._check(self.lib.ref_memory_report(classes, window, int(double), local, out))
+        return dict(b_bytes=out[0], c_bytes=out[1], d_bytes=out[2], total_bytes=out[3])
+
+    # ---- L-JSDE
+    def reconstruct_algo(self, frame, opaque, period, algo, window=32, block=4, iterations=200,
+                         step=0.5, clip=False, threads=0):
+        frame = np.ascontiguousarray(frame, np.float64)
+        out = np.zeros((2 * frame.shape[0], 2 * frame.shape[1]))
+        sec = C.c_double()
+        self._check(self.lib.ref_reconstruct_algo(
+            _d(frame), frame.shape[0], frame.shape[1],
+            np.ascontiguousarray(opaque, np.uint8).ctypes.data_as(_u8p), period, window, block,
+            iterations, step, 0 if algo == "ljsde" else 1, int(clip), threads, _d(out),
+            C.byref(sec)))
+        return out, sec.value
+
+    def ljsde_trace(self, opaque, period, orow, ocol, window, y, iterations=200, step=0.5):
+        n = max(iterations, 1)
+        picks = np.full(n, -1, np.int32)
+        gd = np.zeros(2 * n)
+        win = np.zeros(window * window)
+        y = np.ascontiguousarray(y, np.float64)
+        k = self._check(self.lib.ref_ljsde_trace(
+            np.ascontiguousarray(opaque, np.uint8).ctypes.data_as(_u8p), period, orow, ocol,
+            window, _d(y), iterations, step, picks.ctypes.data_as(_ip), _d(gd), _d(win)))
+        return picks[:k], (gd[0::2] + 1j * gd[1::2])[:k], win.reshape(window, window)
 
     def _check(self, rc):
         if rc < 0:

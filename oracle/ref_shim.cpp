@@ -15,13 +15,23 @@
 //                                                            rljsde.cpp:186-201)
 //   ref_block_trace       -> tqs::rljsde_block with an IterationHook (rljsde.cpp:258-271)
 //   ref_frequency_weights -> tqs::frequency_weights         (basis.cpp:99-106)
+//   ref_io_*              -> tqs::read_pgm / write_pgm / read_pattern / write_pattern /
+//                            read_frame / write_raw_image / read_image_any (io.cpp)
+//   ref_pattern_digest, ref_save_cache, ref_load_cache
+//                         -> tqs::pattern_digest / save_kernel_cache / load_kernel_cache
+//                                                           (rljsde.cpp:337-475)
+//   ref_memory_report     -> tqs::kernel_memory_report      (rljsde.cpp:322-335)
+//   ref_reconstruct_algo  -> tqs::reconstruct with Algorithm::Ljsde or Rljsde
+//   ref_ljsde_trace       -> tqs::ljsde_block with an IterationHook (ljsde.cpp:131-185)
 // Exceptions never cross the ABI: they become a negative return code and the
 // message is kept for ref_last_error().
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
+#include <span>
 #include <string>
 #include <thread>
 #include <vector>
@@ -29,6 +39,8 @@
 #include "synthetic.hpp"
 #include "tqs/basis.hpp"
 #include "tqs/grid.hpp"
+#include "tqs/io.hpp"
+#include "tqs/ljsde.hpp"
 #include "tqs/pipeline.hpp"
 #include "tqs/rljsde.hpp"
 
@@ -252,6 +264,189 @@ int ref_block_trace(const uint8_t* opaque, int period, int origin_row, int origi
                 gd[2 * n] = g.real();
                 gd[2 * n + 1] = g.imag();
                 ++n;
+            });
+        std::memcpy(window_out, win.data(), win.size() * sizeof(double));
+        return n;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, -1);
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+// ---------------------------------------------------------------- file formats
+int ref_io_write_pgm(const char* path, const double* img, int rows, int cols, int bits) {
+    try {
+        tqs::Image im(rows, cols);
+        if (rows > 0 && cols > 0) std::memcpy(im.values.data(), img, im.values.size() * sizeof(double));
+        tqs::write_pgm(path, im, bits);
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, -1);
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+// kind 0: read_image_any, 1: read_pgm, 2: read_frame (TQSM)
+int ref_io_read(const char* path, int kind, int* rows, int* cols, double* out) {
+    try {
+        std::vector<double> v;
+        if (kind == 2) {
+            const tqs::MeasurementFrame f = tqs::read_frame(path);
+            *rows = f.rows, *cols = f.cols, v = f.values;
+        } else {
+            const tqs::Image im = kind == 1 ? tqs::read_pgm(path) : tqs::read_image_any(path);
+            *rows = im.rows, *cols = im.cols, v = im.values;
+        }
+        if (out) std::memcpy(out, v.data(), v.size() * sizeof(double));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, -1);
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+int ref_io_write_tqsm(const char* path, const double* v, int rows, int cols) {
+    try {
+        tqs::Image im(rows, cols);
+        std::memcpy(im.values.data(), v, im.values.size() * sizeof(double));
+        tqs::write_raw_image(path, im);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+int ref_io_write_pattern(const char* path, int period, uint64_t seed, const char* rng,
+                         const uint8_t* opaque) {
+    try {
+        tqs::QuadrantPattern p = make_pattern(opaque, period);
+        p.seed = seed;
+        p.rng = rng;
+        tqs::write_pattern(path, p);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+int ref_io_read_pattern(const char* path, int* period, uint64_t* seed, char* rng, size_t cap,
+                        uint8_t* opaque) {
+    try {
+        const tqs::QuadrantPattern p = tqs::read_pattern(path);
+        *period = p.period;
+        *seed = p.seed;
+        std::snprintf(rng, cap, "%s", p.rng.c_str());
+        if (opaque) std::memcpy(opaque, p.opaque.data(), p.opaque.size());
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, -1);
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+// ---------------------------------------------------------------- TQSK persistence
+uint64_t ref_pattern_digest(const uint8_t* opaque, int period) {
+    return tqs::pattern_digest(make_pattern(opaque, period));
+}
+
+static tqs::KernelCacheHeader cache_header(const uint8_t* opaque, int period, int window,
+                                           int precision_double, double decay, double exponent) {
+    tqs::KernelCacheHeader h;
+    h.window = window;
+    h.period = period;
+    h.precision = precision_double ? tqs::Precision::Double : tqs::Precision::Single;
+    h.weighting.spatialDecay = decay;
+    h.weighting.frequencyExponent = exponent;
+    h.patternDigest = tqs::pattern_digest(make_pattern(opaque, period));
+    return h;
+}
+
+int ref_save_cache(void* cache, const char* path, const uint8_t* opaque, int period, int window,
+                   int precision_double, double decay, double exponent) {
+    try {
+        tqs::save_kernel_cache(path, *static_cast<tqs::KernelCache*>(cache),
+                               cache_header(opaque, period, window, precision_double, decay, exponent));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+int ref_load_cache(void* cache, const char* path, const uint8_t* opaque, int period, int window,
+                   int precision_double, double decay, double exponent) {
+    try {
+        tqs::load_kernel_cache(path, *static_cast<tqs::KernelCache*>(cache),
+                               cache_header(opaque, period, window, precision_double, decay, exponent));
+        return static_cast<int>(static_cast<tqs::KernelCache*>(cache)->classCount());
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+int ref_memory_report(int classes, int window, int precision_double, int local, uint64_t out[4]) {
+    try {
+        const tqs::MemoryReport r = tqs::kernel_memory_report(
+            classes, window, precision_double ? tqs::Precision::Double : tqs::Precision::Single, local);
+        out[0] = r.bBytes, out[1] = r.cBytes, out[2] = r.dBytes, out[3] = r.totalBytes;
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, -1);
+    }
+}
+
+// ---------------------------------------------------------------- L-JSDE
+// tqs::reconstruct with an explicit algorithm (0 = Ljsde, 1 = Rljsde), unclipped
+// or clipped, no external cache.
+int ref_reconstruct_algo(const double* frame, int frame_rows, int frame_cols, const uint8_t* opaque,
+                         int period, int window, int block, int iterations, double step_width,
+                         int algo, int clip, int threads, double* out, double* seconds) {
+    try {
+        tqs::MeasurementFrame f(frame_rows, frame_cols);
+        std::memcpy(f.values.data(), frame, f.values.size() * sizeof(double));
+        tqs::ReconstructionConfig cfg;
+        cfg.window = window;
+        cfg.block = block;
+        cfg.solver.maxIterations = iterations;
+        cfg.solver.stepWidth = step_width;
+        cfg.clipOutput = clip != 0;
+        cfg.algorithm = algo == 0 ? tqs::Algorithm::Ljsde : tqs::Algorithm::Rljsde;
+        cfg.threads = threads;
+        const tqs::ReconstructionReport r = tqs::reconstruct(f, make_pattern(opaque, period), cfg);
+        std::memcpy(out, r.output.values.data(), r.output.values.size() * sizeof(double));
+        if (seconds) *seconds = r.seconds;
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, -1);
+    } catch (const std::exception& e) {
+        return fail(e, -2);
+    }
+}
+
+// ljsde_block on the window at (origin_row, origin_col) with the reference's local
+// system and weights: picks / scaled deltas per iteration and the W*W synthesis.
+int ref_ljsde_trace(const uint8_t* opaque, int period, int origin_row, int origin_col, int window,
+                    const double* y_local, int iterations, double step_width, int* picks,
+                    double* gd, double* window_out) {
+    try {
+        const tqs::QuadrantPattern p = make_pattern(opaque, period);
+        const tqs::LocalMeasurementMatrix A = tqs::extract_local_matrix(p, origin_row, origin_col, window);
+        const std::vector<double> w = tqs::spatial_weights(A, tqs::WeightingConfig{});
+        const std::vector<double> q = tqs::frequency_weights(window, tqs::WeightingConfig{});
+        tqs::SolverOptions opt;
+        opt.maxIterations = iterations;
+        opt.stepWidth = step_width;
+        int n = 0;
+        const std::vector<double> y(y_local, y_local + A.localCount());
+        const std::vector<double> win = tqs::ljsde_block(
+            y, A, w, q, opt, [&](int it, int u, tqs::cplx g, std::span<const tqs::cplx>) {
+                picks[it] = u;
+                gd[2 * it] = g.real();
+                gd[2 * it + 1] = g.imag();
+                n = it + 1;
             });
         std::memcpy(window_out, win.data(), win.size() * sizeof(double));
         return n;

@@ -28,7 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # TQSB_LIB selects an experiment variant built by build.py (default: the product library)
 LIB_PATH = os.environ.get("TQSB_LIB") or os.path.join(HERE, "libtqsb.so")
 
-TQSB_OK, TQSB_EINVAL, TQSB_ECUDA, TQSB_ENOMEM, TQSB_ELOGIC, TQSB_ENODEV = range(6)
+TQSB_OK, TQSB_EINVAL, TQSB_ECUDA, TQSB_ENOMEM, TQSB_ELOGIC, TQSB_ENODEV, TQSB_EIO = range(7)
 
 
 class TqsbError(RuntimeError):
@@ -41,6 +41,10 @@ class NoDeviceError(TqsbError):
 
 class LogicError(RuntimeError):
     """std::logic_error (pipeline.cpp:146-147)."""
+
+
+class FormatError(RuntimeError):
+    """File-format / I/O failure (std::runtime_error "<path>: <what>", io.cpp:15-31)."""
 
 
 class _Config(C.Structure):
@@ -72,6 +76,8 @@ EXPORTS = [
     "tqsb_generate_pattern", "tqsb_simulate", "tqsb_synthetic_image", "tqsb_psnr",
     "tqsb_host_alloc", "tqsb_host_free", "tqsb_device_count", "tqsb_probe_peaks",
     "tqsb_reconstruct_batch",
+    "tqsb_io_read", "tqsb_io_write_pgm", "tqsb_io_write_tqsm", "tqsb_io_read_pattern",
+    "tqsb_io_write_pattern",
 ]
 
 
@@ -117,6 +123,12 @@ def _load() -> C.CDLL:
     L.tqsb_probe_peaks.argtypes = [C.c_int, _dp, _dp]
     L.tqsb_reconstruct_batch.argtypes = [C.c_void_p, C.POINTER(_dp), C.c_int, C.c_int, C.c_int,
                                          C.POINTER(_dp), C.POINTER(_Report)]
+    L.tqsb_io_read.argtypes = [C.c_char_p, C.c_int, _ip, _ip, _dp]
+    L.tqsb_io_write_pgm.argtypes = [C.c_char_p, _dp, C.c_int, C.c_int, C.c_int]
+    L.tqsb_io_write_tqsm.argtypes = [C.c_char_p, _dp, C.c_int, C.c_int]
+    L.tqsb_io_read_pattern.argtypes = [C.c_char_p, _ip, C.POINTER(C.c_uint64), C.c_char_p,
+                                       C.c_size_t, _u8p]
+    L.tqsb_io_write_pattern.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_char_p, _u8p]
     return L
 
 
@@ -133,6 +145,8 @@ def _check(rc: int) -> None:
         raise LogicError(msg)
     if rc == TQSB_ENODEV:
         raise NoDeviceError(msg)
+    if rc == TQSB_EIO:
+        raise FormatError(msg)
     raise TqsbError(msg)
 
 
@@ -425,3 +439,7 @@ def reconstruct_image(image: np.ndarray, pattern: QuadrantPattern, config: Recon
     rep.output = np.ascontiguousarray(rep.output[:r0, :c0])
     rep.psnr_db = psnr(image, rep.output)
     return rep
+
+
+from .io import (read_frame, read_image_any, read_pattern, read_pgm, read_raw_image,  # noqa: E402
+                 write_frame, write_pattern, write_pgm, write_raw_image)

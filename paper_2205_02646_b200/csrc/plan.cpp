@@ -1317,3 +1317,6 @@ int tqsb_probe_peaks(int device, double* fp32_tflops, double* smem_tbps) {
 }
 
 } // extern "C"
+
+// error reporting shared with io.cpp / tqsk handling (same thread-local message)
+int tqsb_internal_set_error(int code, const std::string& msg) { return set_error(code, msg); }
