@@ -74,7 +74,7 @@ struct WeightingConfig {
 struct SolverOptions {
     int maxIterations = 200;
     double stepWidth = 0.5;
-    bool earlyStop = false;  // L-JSDE only in the reference; rejected here when set
+    bool earlyStop = false;  // L-JSDE only (basis.hpp:80-81); ignored by RL-JSDE like the reference
     double earlyStopScale = 1e-14;
 };
 
@@ -132,6 +132,9 @@ inline tqsb_config to_c(const ReconstructionConfig& c) {
     k.threads = c.threads;
     k.compute = c.compute == Compute::Fp64 ? TQSB_COMPUTE_FP64 : TQSB_COMPUTE_FP32;
     k.hot_columns = c.hotColumns;
+    k.algorithm = c.algorithm == Algorithm::Ljsde ? TQSB_ALGO_LJSDE : TQSB_ALGO_RLJSDE;
+    k.early_stop = c.solver.earlyStop ? 1 : 0;
+    k.early_stop_scale = c.solver.earlyStopScale;
     return k;
 }
 }  // namespace detail
@@ -188,13 +191,12 @@ inline ReconstructionReport reconstruct(const MeasurementFrame& frame, const Qua
                                         const Image* reference = nullptr) {
     const tqsb_config k = detail::to_c(config);
     detail::check(tqsb_validate_config(&k, pattern.period));
-    if (config.algorithm != Algorithm::Rljsde)
-        throw std::invalid_argument("only the RL-JSDE algorithm runs on the device");
     if (frame.rows < 1 || frame.cols < 1) throw std::invalid_argument("empty measurement frame");
     if (reference && (reference->rows != 2 * frame.rows || reference->cols != 2 * frame.cols))
         throw std::invalid_argument("reference dimensions do not match the reconstruction");
+    // the reference shares its cache with RL-JSDE only (pipeline.cpp:111-112)
     KernelCache local;
-    KernelCache* kc = cache ? cache : &local;
+    KernelCache* kc = cache && config.algorithm == Algorithm::Rljsde ? cache : &local;
     tqsb_plan* plan = kc->bind(pattern, config);
     ReconstructionReport rep;
     rep.output = Image(2 * frame.rows, 2 * frame.cols);

@@ -44,6 +44,12 @@ extern "C" {
 #define TQSB_COMPUTE_FP32 0
 #define TQSB_COMPUTE_FP64 1
 
+/* Reference Algorithm (pipeline.hpp:15): L-JSDE is the baseline block solver
+ * (ljsde.cpp, re-summed every iteration, always fp64 on the device); RL-JSDE the
+ * recurrent solver (the product path). */
+#define TQSB_ALGO_LJSDE 0
+#define TQSB_ALGO_RLJSDE 1
+
 /* Mirrors ReconstructionConfig field for field (pipeline.hpp:17-26), with
  * SolverOptions (basis.hpp:77-82) and WeightingConfig (basis.hpp:15-18) inlined.
  * `threads` has no device meaning; the device set is given to tqsb_plan_create. */
@@ -58,7 +64,10 @@ typedef struct tqsb_config {
     int clip_output;           /* default 1 (pipeline.hpp:23) */
     int threads;               /* accepted and validated (>= 0) like the reference; unused */
     int compute;               /* TQSB_COMPUTE_*, default FP32 */
-    int hot_columns;           /* shared-memory column cache size; -1 = auto */
+    int hot_columns;           /* C' columns held in tensor memory; -1 = auto */
+    int algorithm;             /* TQSB_ALGO_*, default RLJSDE (pipeline.hpp:15, 25) */
+    int early_stop;            /* L-JSDE energy stop (basis.hpp:80), default 0 */
+    double early_stop_scale;   /* stop once sum_m w_m |r_m|^2 < scale * L (basis.hpp:81), 1e-14 */
 } tqsb_config;
 
 /* Mirrors ReconstructionReport (pipeline.hpp:28-39) minus the output image,
@@ -156,6 +165,22 @@ int tqsb_plan_stats(const tqsb_plan* plan, long long* classes, long long* device
  * c (K*K complex, column-major [uk*K+sk]), d (K). Pass NULL b to query L. */
 int tqsb_plan_export_tables(tqsb_plan* plan, int origin_row, int origin_col, int* local_out,
                             double* b_re, double* b_im, double* c_re, double* c_im, double* d);
+
+/* TQSK table persistence (save_kernel_cache / load_kernel_cache, rljsde.cpp:337-475):
+ * the same header (window, period, precision, spatial decay, frequency exponent,
+ * pattern digest) and per-class planes in the config's precision, so files move
+ * between this library and the reference. save writes every resident class;
+ * load rejects a header that does not match the plan (TQSB_EIO, "<path>: kernel
+ * cache does not match the current configuration") and makes the file's classes
+ * resident on every device of the plan without the fp64 precompute. */
+int tqsb_plan_save_tables(tqsb_plan* plan, const char* path, int* classes_out);
+int tqsb_plan_load_tables(tqsb_plan* plan, const char* path, int* classes_out);
+/* pattern_digest (rljsde.cpp:322-333): FNV-1a over the period's 4 LE bytes, then the
+ * (period/2)^2 quadrant indices. */
+uint64_t tqsb_pattern_digest(const uint8_t* opaque, int period);
+/* kernel_memory_report (rljsde.cpp:322-335): out = {B, C, D, total} bytes of
+ * `classes` table sets (local < 0: W*W/4), TQSB_PRECISION_* storage. */
+int tqsb_kernel_memory_report(int classes, int window, int precision, int local, uint64_t out[4]);
 
 /* Greedy path of one block on the device (parity diagnostics, the analogue of
  * rljsde_block's IterationHook, rljsde.hpp:75-77): y_local (L values, the

@@ -209,7 +209,7 @@ class Reference:
                                            C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _dp,
                                            _dp]
         L.ref_ljsde_trace.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int,
-                                      C.c_double, _ip, _dp, _dp]
+                                      C.c_double, C.c_double, _ip, _dp, _dp]
         self.lib = L
 
     # ---- file formats (tqs::read_* / write_*, io.cpp)
@@ -281,7 +281,8 @@ class Reference:
             C.byref(sec)))
         return out, sec.value
 
-    def ljsde_trace(self, opaque, period, orow, ocol, window, y, iterations=200, step=0.5):
+    def ljsde_trace(self, opaque, period, orow, ocol, window, y, iterations=200, step=0.5,
+                    early_stop_scale=0.0):
         n = max(iterations, 1)
         picks = np.full(n, -1, np.int32)
         gd = np.zeros(2 * n)
@@ -289,7 +290,8 @@ class Reference:
         y = np.ascontiguousarray(y, np.float64)
         k = self._check(self.lib.ref_ljsde_trace(
             np.ascontiguousarray(opaque, np.uint8).ctypes.data_as(_u8p), period, orow, ocol,
-            window, _d(y), iterations, step, picks.ctypes.data_as(_ip), _d(gd), _d(win)))
+            window, _d(y), iterations, step, early_stop_scale, picks.ctypes.data_as(_ip), _d(gd),
+            _d(win)))
         return picks[:k], (gd[0::2] + 1j * gd[1::2])[:k], win.reshape(window, window)
 
     def _check(self, rc):

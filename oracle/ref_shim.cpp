@@ -429,8 +429,8 @@ int ref_reconstruct_algo(const double* frame, int frame_rows, int frame_cols, co
 // ljsde_block on the window at (origin_row, origin_col) with the reference's local
 // system and weights: picks / scaled deltas per iteration and the W*W synthesis.
 int ref_ljsde_trace(const uint8_t* opaque, int period, int origin_row, int origin_col, int window,
-                    const double* y_local, int iterations, double step_width, int* picks,
-                    double* gd, double* window_out) {
+                    const double* y_local, int iterations, double step_width,
+                    double early_stop_scale, int* picks, double* gd, double* window_out) {
     try {
         const tqs::QuadrantPattern p = make_pattern(opaque, period);
         const tqs::LocalMeasurementMatrix A = tqs::extract_local_matrix(p, origin_row, origin_col, window);
@@ -439,6 +439,8 @@ int ref_ljsde_trace(const uint8_t* opaque, int period, int origin_row, int origi
         tqs::SolverOptions opt;
         opt.maxIterations = iterations;
         opt.stepWidth = step_width;
+        opt.earlyStop = early_stop_scale > 0.0;  // <= 0: no energy stop
+        if (opt.earlyStop) opt.earlyStopScale = early_stop_scale;
         int n = 0;
         const std::vector<double> y(y_local, y_local + A.localCount());
         const std::vector<double> win = tqs::ljsde_block(

@@ -52,7 +52,8 @@ class _Config(C.Structure):
                 ("step_width", C.c_double), ("spatial_decay", C.c_double),
                 ("frequency_exponent", C.c_double), ("precision", C.c_int),
                 ("clip_output", C.c_int), ("threads", C.c_int), ("compute", C.c_int),
-                ("hot_columns", C.c_int)]
+                ("hot_columns", C.c_int), ("algorithm", C.c_int), ("early_stop", C.c_int),
+                ("early_stop_scale", C.c_double)]
 
 
 class _Report(C.Structure):
@@ -77,7 +78,8 @@ EXPORTS = [
     "tqsb_host_alloc", "tqsb_host_free", "tqsb_device_count", "tqsb_probe_peaks",
     "tqsb_reconstruct_batch",
     "tqsb_io_read", "tqsb_io_write_pgm", "tqsb_io_write_tqsm", "tqsb_io_read_pattern",
-    "tqsb_io_write_pattern",
+    "tqsb_io_write_pattern", "tqsb_plan_save_tables", "tqsb_plan_load_tables",
+    "tqsb_pattern_digest", "tqsb_kernel_memory_report",
 ]
 
 
@@ -129,6 +131,12 @@ def _load() -> C.CDLL:
     L.tqsb_io_read_pattern.argtypes = [C.c_char_p, _ip, C.POINTER(C.c_uint64), C.c_char_p,
                                        C.c_size_t, _u8p]
     L.tqsb_io_write_pattern.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_char_p, _u8p]
+    L.tqsb_plan_save_tables.argtypes = [C.c_void_p, C.c_char_p, _ip]
+    L.tqsb_plan_load_tables.argtypes = [C.c_void_p, C.c_char_p, _ip]
+    L.tqsb_pattern_digest.argtypes = [_u8p, C.c_int]
+    L.tqsb_pattern_digest.restype = C.c_uint64
+    L.tqsb_kernel_memory_report.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.POINTER(C.c_uint64)]
     return L
 
 
@@ -156,6 +164,7 @@ def _d(a: np.ndarray):
 
 COMPUTE_FP32, COMPUTE_FP64 = 0, 1
 PRECISION_SINGLE, PRECISION_DOUBLE = 0, 1
+ALGO_LJSDE, ALGO_RLJSDE = 0, 1
 
 
 @dataclasses.dataclass
@@ -172,11 +181,15 @@ class ReconstructionConfig:
     threads: int = 1
     compute: int = COMPUTE_FP32
     hot_columns: int = -1
+    algorithm: int = ALGO_RLJSDE
+    early_stop: bool = False
+    early_stop_scale: float = 1e-14
 
     def _c(self) -> _Config:
         return _Config(self.window, self.block, self.max_iterations, self.step_width,
                        self.spatial_decay, self.frequency_exponent, self.precision,
-                       int(self.clip_output), self.threads, self.compute, self.hot_columns)
+                       int(self.clip_output), self.threads, self.compute, self.hot_columns,
+                       self.algorithm, int(self.early_stop), self.early_stop_scale)
 
 
 @dataclasses.dataclass
@@ -250,6 +263,20 @@ def census(frame_rows: int, frame_cols: int, config: ReconstructionConfig, perio
     out = (C.c_longlong * 3)()
     _check(lib.tqsb_census(frame_rows, frame_cols, C.byref(c), period, out))
     return dict(blocks=out[0], classes_total=out[1], classes_interior=out[2])
+
+
+def pattern_digest(pattern: QuadrantPattern) -> int:
+    """FNV-1a content digest of a pattern (rljsde.cpp:322-333), pinned in TQSK headers."""
+    opq = np.ascontiguousarray(pattern.opaque, np.uint8)
+    return lib.tqsb_pattern_digest(opq.ctypes.data_as(_u8p), pattern.period)
+
+
+def kernel_memory_report(classes: int, window: int, precision: int = PRECISION_DOUBLE,
+                         local: int = -1) -> dict:
+    """Byte accounting of `classes` table sets (kernel_memory_report, rljsde.cpp:322-335)."""
+    out = (C.c_uint64 * 4)()
+    _check(lib.tqsb_kernel_memory_report(classes, window, precision, local, out))
+    return dict(b_bytes=out[0], c_bytes=out[1], d_bytes=out[2], total_bytes=out[3])
 
 
 def device_count() -> int:
@@ -385,6 +412,18 @@ class Plan:
         _check(lib.tqsb_plan_export_tables(self._h, origin_row, origin_col, C.byref(L2), _d(bre),
                                            _d(bim), _d(cre), _d(cim), _d(d)))
         return dict(L=L, b=(bre + 1j * bim).reshape(K, L), c=(cre + 1j * cim).reshape(K, K), d=d)
+
+    def save_tables(self, path) -> int:
+        """TQSK file of every resident class (save_kernel_cache, rljsde.cpp:398-432)."""
+        n = C.c_int()
+        _check(lib.tqsb_plan_save_tables(self._h, os.fsencode(path), C.byref(n)))
+        return n.value
+
+    def load_tables(self, path) -> int:
+        """Make a TQSK file's classes resident (load_kernel_cache, rljsde.cpp:434-475)."""
+        n = C.c_int()
+        _check(lib.tqsb_plan_load_tables(self._h, os.fsencode(path), C.byref(n)))
+        return n.value
 
     def block_trace(self, origin_row: int, origin_col: int, y_local: np.ndarray):
         it = max(1, self.config.max_iterations)

@@ -80,6 +80,8 @@ int validate(const tqsb_config& c, int period) {
         return set_error(TQSB_EINVAL, "unknown compute mode");
     if (c.precision != TQSB_PRECISION_SINGLE && c.precision != TQSB_PRECISION_DOUBLE)
         return set_error(TQSB_EINVAL, "unknown precision");
+    if (c.algorithm != TQSB_ALGO_LJSDE && c.algorithm != TQSB_ALGO_RLJSDE)
+        return set_error(TQSB_EINVAL, "unknown algorithm");
     return TQSB_OK;
 }
 
@@ -414,6 +416,77 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     for (auto& t : th) t.join();
 }
 
+// Allocate the device slab of one class (fp64 planes, fp32 product tables, local
+// system) on device d, upload its local system and register it under `key`;
+// cb receives the build descriptor.
+int alloc_class(tqsb_plan* p, Device* d, int key, int orow, int ocol, ClassBuild* cb) {
+    const WindowTables& t = p->wt;
+    const size_t K = t.K, K_pad = t.K_pad, W = t.W;
+    LocalSystem ls = local_system(p->opaque, p->period, orow, ocol, p->cfg);
+    const size_t L = ls.L;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    const size_t o_c64 = take(K * K * 2 * 8), o_b64 = take(K * L * 2 * 8),
+                 o_t64 = take(K * L * 2 * 8), o_d64 = take(K * 8),
+                 o_cpack = take(K_pad * K_pad * 8), o_scale = take(K_pad * 4),
+                 o_fac = take(K_pad * 4), o_mask = take(W * W * 4), o_px = take(L * 6 + 8),
+                 o_w = take(L * 8 + 8);
+    ClassSlab slab;
+    slab.bytes = off;
+    CUDA_TRY(cudaMalloc(&slab.base, slab.bytes));
+    char* b = static_cast<char*>(slab.base);
+    CUDA_TRY(cudaMemcpyAsync(b + o_px, ls.px.data(), L * 6, cudaMemcpyHostToDevice, d->stream));
+    CUDA_TRY(cudaMemcpyAsync(b + o_w, ls.w.data(), L * 8, cudaMemcpyHostToDevice, d->stream));
+    CUDA_TRY(cudaMemcpyAsync(b + o_mask, ls.mask32.data(), W * W * 4, cudaMemcpyHostToDevice,
+                             d->stream));
+    CUDA_TRY(cudaStreamSynchronize(d->stream));  // host vectors die at scope end
+    *cb = ClassBuild{};
+    cb->local = int(L);
+    cb->px = reinterpret_cast<const signed char*>(b + o_px);
+    cb->w = reinterpret_cast<const double*>(b + o_w);
+    cb->t64 = reinterpret_cast<double*>(b + o_t64);
+    cb->b64 = reinterpret_cast<double*>(b + o_b64);
+    cb->c64 = reinterpret_cast<double*>(b + o_c64);
+    cb->d64 = reinterpret_cast<double*>(b + o_d64);
+    cb->cpack = reinterpret_cast<float*>(b + o_cpack);
+    cb->scale = reinterpret_cast<float*>(b + o_scale);
+    cb->fac = reinterpret_cast<float*>(b + o_fac);
+    ClassTab tab{};
+    tab.cpack = cb->cpack;
+    tab.scale = cb->scale;
+    tab.fac = cb->fac;
+    tab.mask32 = reinterpret_cast<const float*>(b + o_mask);
+    tab.b64 = cb->b64;
+    tab.c64 = cb->c64;
+    tab.d64 = cb->d64;
+    tab.cells = nullptr;
+    tab.w64 = cb->w;
+    tab.local = int(L);
+    d->slot_of[key] = int(d->tabs.size());
+    d->tabs.push_back(tab);
+    d->slabs.push_back(slab);
+    d->table_bytes += slab.bytes;
+    return TQSB_OK;
+}
+
+// refresh the device ClassTab array after classes were added
+int publish_tabs(Device* d) {
+    if (d->tabs.size() > d->d_tabs_cap) {
+        CUDA_TRY(cudaStreamSynchronize(d->stream));
+        cudaFree(d->d_tabs);
+        d->d_tabs_cap = std::max<size_t>(d->tabs.size() * 2, 16);
+        CUDA_TRY(cudaMalloc(&d->d_tabs, sizeof(ClassTab) * d->d_tabs_cap));
+    }
+    CUDA_TRY(cudaMemcpyAsync(d->d_tabs, d->tabs.data(), sizeof(ClassTab) * d->tabs.size(),
+                             cudaMemcpyHostToDevice, d->stream));
+    CUDA_TRY(cudaStreamSynchronize(d->stream));
+    return TQSB_OK;
+}
+
 // Build the tables of every class in `keys` that is not resident on device d
 // (batched; the serial warm pass of pipeline.cpp:127-133). Returns the number of
 // classes created through *created.
@@ -425,80 +498,21 @@ int ensure_classes(tqsb_plan* p, Device* d, const std::vector<int>& keys,
     *created = int(missing.size());
     if (missing.empty()) return TQSB_OK;
     CUDA_TRY(cudaSetDevice(d->id));
-    const WindowTables& t = p->wt;
-    const size_t K = t.K, K_pad = t.K_pad, W = t.W;
-    const bool f32 = true;  // fp32 tables are always built (fp64 planes are kept too)
     std::vector<ClassBuild> descs;
     int max_local = 1;
     for (int key : missing) {
         const auto [orow, ocol] = rep.at(key);
-        LocalSystem ls = local_system(p->opaque, p->period, orow, ocol, p->cfg);
-        const size_t L = ls.L;
-        max_local = std::max<int>(max_local, int(L));
-        // slab layout
-        size_t off = 0;
-        auto take = [&](size_t bytes) {
-            size_t o = off;
-            off = align_up(off + bytes, 256);
-            return o;
-        };
-        const size_t o_c64 = take(K * K * 2 * 8), o_b64 = take(K * L * 2 * 8),
-                     o_t64 = take(K * L * 2 * 8), o_d64 = take(K * 8),
-                     o_cpack = take(f32 ? K_pad * K_pad * 8 : 0), o_scale = take(K_pad * 4),
-                     o_fac = take(K_pad * 4), o_mask = take(W * W * 4), o_px = take(L * 6 + 8),
-                     o_w = take(L * 8 + 8);
-        ClassSlab slab;
-        slab.bytes = off;
-        CUDA_TRY(cudaMalloc(&slab.base, slab.bytes));
-        char* b = static_cast<char*>(slab.base);
-        CUDA_TRY(cudaMemcpyAsync(b + o_px, ls.px.data(), L * 6, cudaMemcpyHostToDevice, d->stream));
-        CUDA_TRY(cudaMemcpyAsync(b + o_w, ls.w.data(), L * 8, cudaMemcpyHostToDevice, d->stream));
-        CUDA_TRY(cudaMemcpyAsync(b + o_mask, ls.mask32.data(), W * W * 4, cudaMemcpyHostToDevice,
-                                 d->stream));
-        CUDA_TRY(cudaStreamSynchronize(d->stream));  // host vectors die at scope end
-        ClassBuild cb{};
-        cb.local = int(L);
-        cb.px = reinterpret_cast<const signed char*>(b + o_px);
-        cb.w = reinterpret_cast<const double*>(b + o_w);
-        cb.t64 = reinterpret_cast<double*>(b + o_t64);
-        cb.b64 = reinterpret_cast<double*>(b + o_b64);
-        cb.c64 = reinterpret_cast<double*>(b + o_c64);
-        cb.d64 = reinterpret_cast<double*>(b + o_d64);
-        cb.cpack = f32 ? reinterpret_cast<float*>(b + o_cpack) : nullptr;
-        cb.scale = reinterpret_cast<float*>(b + o_scale);
-        cb.fac = reinterpret_cast<float*>(b + o_fac);
+        ClassBuild cb;
+        TQSB_TRY(alloc_class(p, d, key, orow, ocol, &cb));
+        max_local = std::max(max_local, cb.local);
         descs.push_back(cb);
-        ClassTab tab{};
-        tab.cpack = cb.cpack;
-        tab.scale = cb.scale;
-        tab.fac = cb.fac;
-        tab.mask32 = reinterpret_cast<const float*>(b + o_mask);
-        tab.b64 = cb.b64;
-        tab.c64 = cb.c64;
-        tab.d64 = cb.d64;
-        tab.cells = nullptr;
-        tab.local = int(L);
-        d->slot_of[key] = int(d->tabs.size());
-        d->tabs.push_back(tab);
-        d->slabs.push_back(slab);
-        d->table_bytes += slab.bytes;
     }
-    int rc = launch_tables_batch(descs.data(), int(descs.size()), int(W), int(K_pad),
+    int rc = launch_tables_batch(descs.data(), int(descs.size()), p->wt.W, p->wt.K_pad,
                                  p->cfg.step_width, d->d_unit64, d->d_q64, d->d_perm, max_local,
-                                 d->stream, launches);
+                                 d->stream, launches, 0);
     if (rc != 0) return set_error(TQSB_ECUDA, std::string("table build: ") +
                                                   cudaGetErrorString(cudaError_t(rc)));
-    // refresh the device ClassTab array
-    if (d->tabs.size() > d->d_tabs_cap) {
-        CUDA_TRY(cudaStreamSynchronize(d->stream));
-        cudaFree(d->d_tabs);
-        d->d_tabs_cap = std::max<size_t>(d->tabs.size() * 2, 16);
-        CUDA_TRY(cudaMalloc(&d->d_tabs, sizeof(ClassTab) * d->d_tabs_cap));
-    }
-    CUDA_TRY(cudaMemcpyAsync(d->d_tabs, d->tabs.data(), sizeof(ClassTab) * d->tabs.size(),
-                             cudaMemcpyHostToDevice, d->stream));
-    CUDA_TRY(cudaStreamSynchronize(d->stream));
-    return TQSB_OK;
+    return publish_tabs(d);
 }
 
 // Class-sorted tasks and CTA work items for a band of block rows on device d;
@@ -604,13 +618,15 @@ SolveArgs base_args(tqsb_plan* p, Device* d) {
     a.step = p->cfg.step_width;
     a.clip = p->cfg.clip_output;
     a.hot = d->hot;
+    a.early_stop = p->cfg.early_stop;
+    a.early_stop_scale = p->cfg.early_stop_scale;
     return a;
 }
 
 int launch(tqsb_plan* p, Device* d, const SolveArgs& a, cudaStream_t s) {
-    int rc = p->cfg.compute == TQSB_COMPUTE_FP32
-                 ? launch_solve_f32(a, p->wt.NS, s, d->num_sms)
-                 : launch_solve_f64(a, s, d->num_sms);
+    int rc = p->cfg.algorithm == TQSB_ALGO_LJSDE ? launch_solve_ljsde(a, s, d->num_sms)
+             : p->cfg.compute == TQSB_COMPUTE_FP32 ? launch_solve_f32(a, p->wt.NS, s, d->num_sms)
+                                                   : launch_solve_f64(a, s, d->num_sms);
     if (rc != 0)
         return set_error(TQSB_ECUDA, std::string("solve launch: ") +
                                          cudaGetErrorString(cudaError_t(rc)));
@@ -808,6 +824,15 @@ void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const Geom
     (void)g;
 }
 
+// L-JSDE keeps no kernel cache in the reference (pipeline.cpp:111-112, 173-177):
+// its report carries no cache counters (the device still builds B and D per class)
+void ljsde_report(const tqsb_plan* p, tqsb_report* rep) {
+    if (!rep || p->cfg.algorithm != TQSB_ALGO_LJSDE) return;
+    rep->classes_created = 0;
+    rep->cache_hits = 0;
+    rep->cache_misses = 0;
+}
+
 double psnr_impl(const double* a, const double* b, long long n) {
     double sum = 0.0;
     for (long long i = 0; i < n; ++i) {
@@ -841,6 +866,9 @@ void tqsb_config_default(tqsb_config* c) {
     c->threads = 1;
     c->compute = TQSB_COMPUTE_FP32;
     c->hot_columns = -1;
+    c->algorithm = TQSB_ALGO_RLJSDE;
+    c->early_stop = 0;
+    c->early_stop_scale = 1e-14;
 }
 
 int tqsb_validate_config(const tqsb_config* cfg, int period) {
@@ -951,6 +979,7 @@ int tqsb_reconstruct_band(tqsb_plan* p, const double* frame, int frame_rows, int
     if (rs[0].rc) return set_error(rs[0].rc, rs[0].err);
     fill_report(rep, rs, g, rs[0].classes_total, rs[0].classes_interior,
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    ljsde_report(p, rep);
     return TQSB_OK;
 }
 
@@ -990,6 +1019,7 @@ int tqsb_reconstruct(tqsb_plan* p, const double* frame, int frame_rows, int fram
     }
     const double e2e = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     fill_report(rep, rs, g, ct, ci, e2e);
+    ljsde_report(p, rep);
     if (reference) {
         const double v = psnr_impl(reference, out, (long long)g.M * g.N);
         if (rep) {
@@ -1028,6 +1058,7 @@ int tqsb_reconstruct_batch(tqsb_plan* p, const double* const* frames, int n_fram
         if (r.rc) return set_error(r.rc, r.err);
     const double e2e = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     fill_report(rep, rs, g, rs[0].classes_total, rs[0].classes_interior, e2e);
+    ljsde_report(p, rep);
     return TQSB_OK;
 }
 
@@ -1115,6 +1146,242 @@ int tqsb_plan_export_tables(tqsb_plan* p, int orow, int ocol, int* local_out, do
         c_re[i] = c[2 * i];
         c_im[i] = c[2 * i + 1];
     }
+    return TQSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// TQSK table persistence (rljsde.cpp:337-475): header (window, period, precision,
+// spatial decay, frequency exponent, pattern digest, class count) then, per class in
+// (row, col) order, (row, col, L) and the planes bRe, bIm [k*L+m], cRe, cIm
+// [uk*K+sk], d in the header's precision. Files written here load in the reference
+// and vice versa; loading skips the fp64 precompute (K1) and derives only the fp32
+// product tables on the device.
+// ---------------------------------------------------------------------------
+uint64_t tqsb_pattern_digest(const uint8_t* opaque, int period) {
+    uint64_t h = 14695981039346656037ull;  // FNV-1a over period (LE bytes) then quadrants
+    auto mix = [&h](uint8_t x) {
+        h ^= x;
+        h *= 1099511628211ull;
+    };
+    for (int i = 0; i < 4; ++i) mix(uint8_t(uint32_t(period) >> (8 * i)));
+    if (opaque && period >= 2)
+        for (int i = 0; i < (period / 2) * (period / 2); ++i) mix(opaque[i]);
+    return h;
+}
+
+int tqsb_kernel_memory_report(int classes, int window, int precision, int local, uint64_t out[4]) {
+    if (!out) return set_error(TQSB_EINVAL, "null argument");
+    if (classes < 0 || window <= 0)
+        return set_error(TQSB_EINVAL, "kernel_memory_report: invalid shape");
+    const uint64_t K = uint64_t(window) * window, L = local < 0 ? K / 4 : uint64_t(local);
+    const uint64_t cb = precision == TQSB_PRECISION_SINGLE ? 8 : 16;  // bytes per complex
+    out[0] = uint64_t(classes) * L * K * cb;
+    out[1] = uint64_t(classes) * K * K * cb;
+    out[2] = uint64_t(classes) * K * cb;  // D counted as complex, like the reference
+    out[3] = out[0] + out[1] + out[2];
+    return TQSB_OK;
+}
+
+namespace {
+
+struct TqskWriter {
+    std::FILE* f;
+    bool ok = true;
+    void raw(const void* p, size_t n) { ok = ok && std::fwrite(p, 1, n, f) == n; }
+    void u32(uint32_t v) {
+        unsigned char b[4];
+        for (int i = 0; i < 4; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+        raw(b, 4);
+    }
+    void u64(uint64_t v) {
+        unsigned char b[8];
+        for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+        raw(b, 8);
+    }
+    void f64(double v) {
+        uint64_t u;
+        std::memcpy(&u, &v, 8);
+        u64(u);
+    }
+    // one plane: component `comp` of an interleaved complex array (comp < 0: real array)
+    void plane(const double* v, size_t n, int comp, bool single) {
+        std::vector<unsigned char> buf(n * (single ? 4 : 8));
+        for (size_t i = 0; i < n; ++i) {
+            const double x = comp < 0 ? v[i] : v[2 * i + comp];
+            if (single) {
+                const float y = float(x);
+                uint32_t u;
+                std::memcpy(&u, &y, 4);
+                for (int k = 0; k < 4; ++k) buf[4 * i + k] = static_cast<unsigned char>(u >> (8 * k));
+            } else {
+                uint64_t u;
+                std::memcpy(&u, &x, 8);
+                for (int k = 0; k < 8; ++k) buf[8 * i + k] = static_cast<unsigned char>(u >> (8 * k));
+            }
+        }
+        raw(buf.data(), buf.size());
+    }
+};
+
+struct TqskReader {
+    std::FILE* f;
+    bool ok = true;
+    void raw(void* p, size_t n) { ok = ok && std::fread(p, 1, n, f) == n; }
+    uint64_t le(int n) {
+        unsigned char b[8] = {};
+        raw(b, size_t(n));
+        uint64_t v = 0;
+        for (int i = 0; i < n; ++i) v |= uint64_t(b[i]) << (8 * i);
+        return v;
+    }
+    double f64() {
+        const uint64_t u = le(8);
+        double v;
+        std::memcpy(&v, &u, 8);
+        return v;
+    }
+    // a plane of n values into component `comp` of interleaved `v` (comp < 0: real)
+    void plane(double* v, size_t n, int comp, bool single) {
+        std::vector<unsigned char> buf(n * (single ? 4 : 8));
+        raw(buf.data(), buf.size());
+        if (!ok) return;
+        for (size_t i = 0; i < n; ++i) {
+            double x;
+            if (single) {
+                uint32_t u = 0;
+                for (int k = 0; k < 4; ++k) u |= uint32_t(buf[4 * i + k]) << (8 * k);
+                float y;
+                std::memcpy(&y, &u, 4);
+                x = y;
+            } else {
+                uint64_t u = 0;
+                for (int k = 0; k < 8; ++k) u |= uint64_t(buf[8 * i + k]) << (8 * k);
+                std::memcpy(&x, &u, 8);
+            }
+            (comp < 0 ? v[i] : v[2 * i + comp]) = x;
+        }
+    }
+};
+
+}  // namespace
+
+int tqsb_plan_save_tables(tqsb_plan* p, const char* path, int* classes_out) {
+    if (!p || !path) return set_error(TQSB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    const std::string where(path);
+    // every resident class (union over devices, first holder wins), in key order
+    std::map<int, std::pair<Device*, int>> owner;
+    for (auto& dp : p->devs)
+        for (const auto& [key, slot] : dp->slot_of) owner.emplace(key, std::make_pair(dp.get(), slot));
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) return set_error(TQSB_EIO, where + ": cannot open for writing");
+    TqskWriter w{f};
+    const bool single = p->cfg.precision == TQSB_PRECISION_SINGLE;
+    w.raw("TQSK", 4);
+    w.u32(uint32_t(p->cfg.window));
+    w.u32(uint32_t(p->period));
+    w.u32(single ? 0u : 1u);
+    w.f64(p->cfg.spatial_decay);
+    w.f64(p->cfg.frequency_exponent);
+    w.u64(tqsb_pattern_digest(p->opaque.data(), p->period));
+    w.u32(uint32_t(owner.size()));
+    const size_t K = p->wt.K;
+    std::vector<double> b, c, dv(K);
+    for (const auto& [key, hold] : owner) {
+        Device* d = hold.first;
+        const ClassTab& t = d->tabs[hold.second];
+        const size_t L = size_t(t.local);
+        b.resize(K * L * 2);
+        c.resize(K * K * 2);
+        if (cudaSetDevice(d->id) != cudaSuccess ||
+            cudaMemcpy(b.data(), t.b64, sizeof(double) * b.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(c.data(), t.c64, sizeof(double) * c.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(dv.data(), t.d64, sizeof(double) * K, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            std::fclose(f);
+            return set_error(TQSB_ECUDA, where + ": table download failed");
+        }
+        w.u32(uint32_t(key / p->period));
+        w.u32(uint32_t(key % p->period));
+        w.u32(uint32_t(L));
+        w.plane(b.data(), K * L, 0, single);
+        w.plane(b.data(), K * L, 1, single);
+        w.plane(c.data(), K * K, 0, single);
+        w.plane(c.data(), K * K, 1, single);
+        w.plane(dv.data(), K, -1, single);
+    }
+    const bool closed = std::fclose(f) == 0;
+    if (!w.ok || !closed) return set_error(TQSB_EIO, where + ": write failed");
+    if (classes_out) *classes_out = int(owner.size());
+    return TQSB_OK;
+}
+
+int tqsb_plan_load_tables(tqsb_plan* p, const char* path, int* classes_out) {
+    if (!p || !path) return set_error(TQSB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    const std::string where(path);
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) return set_error(TQSB_EIO, where + ": cannot open for reading");
+    std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, std::fclose);
+    TqskReader r{f};
+    char magic[4] = {};
+    r.raw(magic, 4);
+    if (!r.ok || std::memcmp(magic, "TQSK", 4) != 0)
+        return set_error(TQSB_EIO, where + ": not a TQSK kernel cache");
+    const int window = int(r.le(4)), period = int(r.le(4));
+    const bool single = r.le(4) == 0;
+    const double decay = r.f64(), expo = r.f64();
+    const uint64_t digest = r.le(8);
+    const uint32_t n = uint32_t(r.le(4));
+    if (!r.ok) return set_error(TQSB_EIO, where + ": truncated header");
+    const bool plan_single = p->cfg.precision == TQSB_PRECISION_SINGLE;
+    if (window != p->cfg.window || period != p->period || single != plan_single ||
+        digest != tqsb_pattern_digest(p->opaque.data(), p->period) ||
+        decay != p->cfg.spatial_decay || expo != p->cfg.frequency_exponent)
+        return set_error(TQSB_EIO, where + ": kernel cache does not match the current configuration");
+    const size_t K = size_t(window) * window;
+    int installed = 0;
+    std::vector<double> b, c, dv(K);
+    for (uint32_t i = 0; i < n; ++i) {
+        const int row = int(r.le(4)), col = int(r.le(4));
+        const size_t L = size_t(r.le(4));
+        if (!r.ok || L > K || row < 0 || col < 0 || row >= period || col >= period)
+            return set_error(TQSB_EIO, where + ": corrupt class record");
+        b.assign(K * L * 2, 0.0);
+        c.assign(K * K * 2, 0.0);
+        r.plane(b.data(), K * L, 0, single);
+        r.plane(b.data(), K * L, 1, single);
+        r.plane(c.data(), K * K, 0, single);
+        r.plane(c.data(), K * K, 1, single);
+        r.plane(dv.data(), K, -1, single);
+        if (!r.ok) return set_error(TQSB_EIO, where + ": truncated class payload");
+        const int key = row * period + col;
+        if (local_system(p->opaque, period, row, col, p->cfg).L != int(L))
+            return set_error(TQSB_EIO, where + ": corrupt class record");
+        for (auto& dp : p->devs) {
+            Device* d = dp.get();
+            if (d->slot_of.count(key)) continue;  // already resident: the first insert wins
+            CUDA_TRY(cudaSetDevice(d->id));
+            ClassBuild cb;
+            TQSB_TRY(alloc_class(p, d, key, row, col, &cb));
+            CUDA_TRY(cudaMemcpyAsync(cb.b64, b.data(), sizeof(double) * b.size(),
+                                     cudaMemcpyHostToDevice, d->stream));
+            CUDA_TRY(cudaMemcpyAsync(cb.c64, c.data(), sizeof(double) * c.size(),
+                                     cudaMemcpyHostToDevice, d->stream));
+            CUDA_TRY(cudaMemcpyAsync(cb.d64, dv.data(), sizeof(double) * K, cudaMemcpyHostToDevice,
+                                     d->stream));
+            int launches = 0;
+            const int rc = launch_tables_batch(&cb, 1, window, p->wt.K_pad, p->cfg.step_width,
+                                               d->d_unit64, d->d_q64, d->d_perm, cb.local,
+                                               d->stream, &launches, 1);
+            if (rc != 0)
+                return set_error(TQSB_ECUDA, std::string("table derive: ") +
+                                                 cudaGetErrorString(cudaError_t(rc)));
+            CUDA_TRY(cudaStreamSynchronize(d->stream));  // b/c/dv are reused next record
+            TQSB_TRY(publish_tabs(d));
+        }
+        ++installed;
+    }
+    if (classes_out) *classes_out = installed;
     return TQSB_OK;
 }
 

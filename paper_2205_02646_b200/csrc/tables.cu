@@ -203,7 +203,7 @@ __global__ void k_pack32(const ClassBuild* __restrict__ cls, int W, int k_pad,
 // Batched build over n classes; `descs` is a host array copied to the device here.
 int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, double step,
                         const double* unit64, const double* q64, const int* perm,
-                        int max_local, void* stream_, int* launches) {
+                        int max_local, void* stream_, int* launches, int derived_only) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     const ClassBuild* hd = static_cast<const ClassBuild*>(host_descs);
     ClassBuild* dd = nullptr;
@@ -215,18 +215,21 @@ int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, do
     for (int z0 = 0; z0 < n; z0 += 65535) {
         const int nz = n - z0 < 65535 ? n - z0 : 65535;
         const ClassBuild* d = dd + z0;
-        {
-            dim3 g((max_local + 127) / 128, K, nz);
-            k_transform<<<g, 128, 0, stream>>>(d, window, unit64);
-        }
-        {
-            const int nt = (K + GT - 1) / GT;
-            dim3 g(nt * (nt + 1) / 2, 1, nz);
-            k_gram<<<g, 256, 0, stream>>>(d, window, nt);
-        }
-        {
-            dim3 g((K + 255) / 256, 1, nz);
-            k_diag<<<g, 256, 0, stream>>>(d, window);
+        if (!derived_only) {
+            {
+                dim3 g((max_local + 127) / 128, K, nz);
+                k_transform<<<g, 128, 0, stream>>>(d, window, unit64);
+            }
+            {
+                const int nt = (K + GT - 1) / GT;
+                dim3 g(nt * (nt + 1) / 2, 1, nz);
+                k_gram<<<g, 256, 0, stream>>>(d, window, nt);
+            }
+            {
+                dim3 g((K + 255) / 256, 1, nz);
+                k_diag<<<g, 256, 0, stream>>>(d, window);
+            }
+            if (launches) *launches += 3;
         }
         {
             dim3 g((k_pad + 255) / 256, 1, nz);
@@ -236,7 +239,7 @@ int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, do
             dim3 g((k_pad / 2 + 127) / 128, k_pad, nz);
             k_pack32<<<g, 128, 0, stream>>>(d, window, k_pad, perm, q64);
         }
-        if (launches) *launches += 5;
+        if (launches) *launches += 2;
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

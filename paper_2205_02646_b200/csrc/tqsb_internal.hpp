@@ -43,6 +43,7 @@ struct ClassTab {
     const double* c64;    // K*K complex interleaved, column-major [uk*K+sk]
     const double* d64;    // K
     const int* cells;     // L x (cell frame row offset, cell frame col offset) vs window origin
+    const double* w64;    // L spatial weights (basis.cpp:75-88; L-JSDE residual update)
     int local;            // L
     int pad;
 };
@@ -74,7 +75,9 @@ struct SolveArgs {
     int window, block, iterations;
     double step;
     int clip;
-    int hot;               // columns cached in shared memory (fp32)
+    int hot;               // C' columns in the TMEM tier (fp32)
+    int early_stop;        // L-JSDE energy stop (ljsde.cpp:178-183)
+    double early_stop_scale;
     // tracing (single-block diagnostics): when trace_picks != nullptr, block 0
     // records picks (flat k), gd (re,im) and the full window synthesis.
     int* trace_picks;
@@ -86,6 +89,7 @@ struct SolveArgs {
 // ---- launchers (defined in the .cu files); return cudaError_t as int ----
 int launch_solve_f32(const SolveArgs& a, int n_slots, void* stream, int num_sms);
 int launch_solve_f64(const SolveArgs& a, void* stream, int num_sms);
+int launch_solve_ljsde(const SolveArgs& a, void* stream, int num_sms);
 size_t solve_f32_smem_bytes(int n_slots, int hot);
 int solve_f32_max_hot(int n_slots, int device);
 
@@ -102,9 +106,11 @@ struct ClassBuild {
     float* scale;              // K_pad
     float* fac;                // K_pad
 };
+// derived_only: b64 / c64 / d64 are already on the device (loaded TQSK planes);
+// only the fp32 product tables (k_scale, k_pack32) are derived from them.
 int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, double step,
                         const double* unit64, const double* q64, const int* perm,
-                        int max_local, void* stream, int* launches);
+                        int max_local, void* stream, int* launches, int derived_only);
 
 int probe_peaks(int device, double* fp32_tflops, double* smem_tbps);
 
