@@ -218,6 +218,50 @@ inline ReconstructionReport reconstruct(const MeasurementFrame& frame, const Qua
     return rep;
 }
 
+// ---- kernel-cache persistence and accounting (rljsde.hpp:102-131) ----
+struct KernelCacheHeader {
+    int window = 0;
+    int period = 0;
+    Precision precision = Precision::Double;
+    WeightingConfig weighting;
+    uint64_t patternDigest = 0;
+};
+
+// pattern_digest (rljsde.cpp:322-333)
+inline uint64_t pattern_digest(const QuadrantPattern& pattern) {
+    return tqsb_pattern_digest(pattern.opaque.data(), pattern.period);
+}
+
+// TQSK files (rljsde.cpp:337-475). The device store must be bound to its pattern and
+// config first (KernelCache::bind); the header is validated against that binding.
+inline void save_kernel_cache(const std::string& path, KernelCache& cache, const QuadrantPattern& p,
+                              const ReconstructionConfig& c) {
+    detail::check(tqsb_plan_save_tables(cache.bind(p, c), path.c_str(), nullptr));
+}
+inline size_t load_kernel_cache(const std::string& path, KernelCache& cache, const QuadrantPattern& p,
+                                const ReconstructionConfig& c) {
+    int n = 0;
+    detail::check(tqsb_plan_load_tables(cache.bind(p, c), path.c_str(), &n));
+    return size_t(n);
+}
+
+struct MemoryReport {
+    uint64_t bBytes = 0, cBytes = 0, dBytes = 0, totalBytes = 0;
+    double bMegabytes() const { return double(bBytes) / 1e6; }
+    double cMegabytes() const { return double(cBytes) / 1e6; }
+    double dMegabytes() const { return double(dBytes) / 1e6; }
+    double totalMegabytes() const { return double(totalBytes) / 1e6; }
+};
+
+// kernel_memory_report (rljsde.cpp:322-335)
+inline MemoryReport kernel_memory_report(int classes, int window, Precision precision, int local = -1) {
+    uint64_t o[4];
+    detail::check(tqsb_kernel_memory_report(
+        classes, window, precision == Precision::Single ? TQSB_PRECISION_SINGLE : TQSB_PRECISION_DOUBLE,
+        local, o));
+    return MemoryReport{o[0], o[1], o[2], o[3]};
+}
+
 // generate_pattern (grid.cpp:8-26)
 inline QuadrantPattern generate_pattern(uint64_t seed, int period, int blockSize = 4) {
     QuadrantPattern p;

@@ -76,7 +76,23 @@ def build(verbose: bool = False, defines: list[str] | None = None, lib: str | No
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs,
               "-Xcompiler", "-pthread"])
         os.replace(lib + ".tmp", lib)
+    if lib == LIB:
+        build_cli(lib)
     return lib
+
+
+def build_cli(lib: str = LIB) -> str:
+    """bin/tqsb: the command-line toolbox (csrc/cli/tqsb_cli.cpp) over libtqsb.so."""
+    src = os.path.join(CSRC, "cli", "tqsb_cli.cpp")
+    out = os.path.join(HERE, "bin", "tqsb")
+    deps = [src, lib, os.path.join(INCLUDE, "tqsb", "reconstruct.hpp"),
+            os.path.join(INCLUDE, "tqsb", "io.hpp"), os.path.join(INCLUDE, "tqsb", "tqsb.h")]
+    if _newer(out, deps):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        _run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", INCLUDE, src, "-L", HERE,
+              "-l:" + os.path.basename(lib), "-Wl,-rpath,$ORIGIN/..", "-o", out + ".tmp"])
+        os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
