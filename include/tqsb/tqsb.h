@@ -199,6 +199,15 @@ int tqsb_simulate(const double* image, int rows, int cols, const uint8_t* opaque
                   double* frame_out);
 /* synthetic test image (tests/support/synthetic.cpp:9-80), values in [0.02, 0.98]. */
 int tqsb_synthetic_image(int rows, int cols, uint64_t seed, double* out);
+/* Input side on the device (no host round trip): the synthetic scene evaluated on
+ * `device` into d_out (rows x cols float64; parameters drawn like the host version,
+ * pixels within a few ulp of it), and the plan's sensor readout of a device image
+ * (simulate_measurement, grid.cpp:46-66; image rows x cols even -> frame
+ * rows/2 x cols/2 in d_frame) on the plan's first device. Asynchronous on `stream`. */
+int tqsb_synthetic_image_device(int device, int rows, int cols, uint64_t seed, double* d_out,
+                                void* stream);
+int tqsb_plan_simulate_device(tqsb_plan* plan, const double* d_image, int rows, int cols,
+                              double* d_frame, void* stream);
 /* psnr (pipeline.cpp:221-233): +inf when identical. */
 double tqsb_psnr(const double* reference, const double* estimate, long long n);
 

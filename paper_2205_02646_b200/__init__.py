@@ -79,7 +79,8 @@ EXPORTS = [
     "tqsb_reconstruct_batch",
     "tqsb_io_read", "tqsb_io_write_pgm", "tqsb_io_write_tqsm", "tqsb_io_read_pattern",
     "tqsb_io_write_pattern", "tqsb_plan_save_tables", "tqsb_plan_load_tables",
-    "tqsb_pattern_digest", "tqsb_kernel_memory_report",
+    "tqsb_pattern_digest", "tqsb_kernel_memory_report", "tqsb_synthetic_image_device",
+    "tqsb_plan_simulate_device",
 ]
 
 
@@ -137,6 +138,10 @@ def _load() -> C.CDLL:
     L.tqsb_pattern_digest.restype = C.c_uint64
     L.tqsb_kernel_memory_report.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int,
                                             C.POINTER(C.c_uint64)]
+    L.tqsb_synthetic_image_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p,
+                                              C.c_void_p]
+    L.tqsb_plan_simulate_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                            C.c_void_p]
     return L
 
 
@@ -243,6 +248,13 @@ def synthetic_image(rows: int, cols: int, seed: int) -> np.ndarray:
     out = np.zeros((rows, cols))
     _check(lib.tqsb_synthetic_image(rows, cols, seed, _d(out)))
     return out
+
+
+def synthetic_image_device(rows: int, cols: int, seed: int, d_out_ptr: int, device: int = 0,
+                           stream: int = 0) -> None:
+    """The synthetic scene evaluated on a device into d_out (rows x cols float64)."""
+    _check(lib.tqsb_synthetic_image_device(device, rows, cols, seed, C.c_void_p(d_out_ptr),
+                                           C.c_void_p(stream)))
 
 
 def psnr(reference: np.ndarray, estimate: np.ndarray) -> float:
@@ -412,6 +424,12 @@ class Plan:
         _check(lib.tqsb_plan_export_tables(self._h, origin_row, origin_col, C.byref(L2), _d(bre),
                                            _d(bim), _d(cre), _d(cim), _d(d)))
         return dict(L=L, b=(bre + 1j * bim).reshape(K, L), c=(cre + 1j * cim).reshape(K, K), d=d)
+
+    def simulate_device(self, d_image_ptr: int, rows: int, cols: int, d_frame_ptr: int,
+                        stream: int = 0) -> None:
+        """Sensor readout of a device image into a device frame (grid.cpp:46-66)."""
+        _check(lib.tqsb_plan_simulate_device(self._h, C.c_void_p(d_image_ptr), rows, cols,
+                                             C.c_void_p(d_frame_ptr), C.c_void_p(stream)))
 
     def save_tables(self, path) -> int:
         """TQSK file of every resident class (save_kernel_cache, rljsde.cpp:398-432)."""

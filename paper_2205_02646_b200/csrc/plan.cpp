@@ -291,6 +291,7 @@ struct Device {
     float* d_unit32 = nullptr;
     double* d_unit64 = nullptr;
     double* d_q64 = nullptr;
+    uint8_t* d_opaque = nullptr;   // the pattern's (P/2)^2 quadrant indices (device readout)
     std::map<int, int> slot_of;    // class key -> slot
     std::vector<ClassTab> tabs;    // host mirror
     std::vector<ClassSlab> slabs;
@@ -346,6 +347,8 @@ int device_init(tqsb_plan* p, Device* d) {
     CUDA_TRY(cudaMalloc(&d->d_unit32, sizeof(float) * 2 * t.W));
     CUDA_TRY(cudaMalloc(&d->d_unit64, sizeof(double) * 2 * t.W));
     CUDA_TRY(cudaMalloc(&d->d_q64, sizeof(double) * t.K));
+    CUDA_TRY(cudaMalloc(&d->d_opaque, p->opaque.size()));
+    CUDA_TRY(cudaMemcpy(d->d_opaque, p->opaque.data(), p->opaque.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_perm, t.perm.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_src, t.src.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_unit32, t.unit32.data(), sizeof(float) * 2 * t.W, cudaMemcpyHostToDevice));
@@ -372,6 +375,7 @@ void device_free(Device* d) {
     cudaFree(d->d_unit32);
     cudaFree(d->d_unit64);
     cudaFree(d->d_q64);
+    cudaFree(d->d_opaque);
     cudaFree(d->d_frame);
     cudaFree(d->d_out);
     if (d->h_in) cudaFreeHost(d->h_in);
@@ -1510,44 +1514,18 @@ int tqsb_simulate(const double* image, int rows, int cols, const uint8_t* opaque
 // (the generator of tests/support/synthetic.cpp:9-80).
 int tqsb_synthetic_image(int rows, int cols, uint64_t seed, double* out) {
     if (!out || rows < 1 || cols < 1) return set_error(TQSB_EINVAL, "invalid image shape");
-    std::mt19937_64 gen(seed);
-    std::uniform_real_distribution<double> U(0.0, 1.0);
+    const SceneParams sp = scene_params(rows, cols, seed);
     const double two_pi = 6.283185307179586;
-    const double ramp_r = U(gen) * 2.0 - 1.0;
-    const double ramp_c = U(gen) * 2.0 - 1.0;
-    double wave[6][4];
-    for (auto& wv : wave) {
-        wv[0] = (U(gen) * 6.0 + 0.5) / rows;
-        wv[1] = (U(gen) * 6.0 + 0.5) / cols;
-        wv[2] = U(gen) * two_pi;
-        wv[3] = U(gen) * 0.5 + 0.1;
-    }
-    double bump[5][4];
-    const double short_side = std::min(rows, cols);
-    for (auto& bp : bump) {
-        bp[0] = U(gen) * rows;
-        bp[1] = U(gen) * cols;
-        bp[2] = (U(gen) * 0.12 + 0.04) * short_side;
-        bp[3] = (U(gen) * 2.0 - 1.0) * 0.8;
-    }
-    double edge[2][4];
-    for (auto& ed : edge) {
-        const double theta = U(gen) * two_pi;
-        ed[0] = std::sin(theta);
-        ed[1] = std::cos(theta);
-        ed[2] = U(gen) * (rows + cols) * 0.5;
-        ed[3] = (U(gen) * 2.0 - 1.0) * 0.6;
-    }
     double vmin = 1e300, vmax = -1e300;
     for (int r = 0; r < rows; ++r)
         for (int c = 0; c < cols; ++c) {
-            double v = ramp_r * r / rows + ramp_c * c / cols;
-            for (const auto& wv : wave) v += wv[3] * std::sin(two_pi * (wv[0] * r + wv[1] * c) + wv[2]);
-            for (const auto& bp : bump) {
+            double v = sp.ramp_r * r / rows + sp.ramp_c * c / cols;
+            for (const auto& wv : sp.wave) v += wv[3] * std::sin(two_pi * (wv[0] * r + wv[1] * c) + wv[2]);
+            for (const auto& bp : sp.bump) {
                 const double dy = r - bp[0], dx = c - bp[1];
                 v += bp[3] * std::exp(-(dy * dy + dx * dx) / (2.0 * bp[2] * bp[2]));
             }
-            for (const auto& ed : edge)
+            for (const auto& ed : sp.edge)
                 v += ed[3] / (1.0 + std::exp(-(ed[0] * r + ed[1] * c - ed[2]) / 2.5));
             out[size_t(r) * cols + c] = v;
             vmin = std::min(vmin, v);
@@ -1555,6 +1533,40 @@ int tqsb_synthetic_image(int rows, int cols, uint64_t seed, double* out) {
         }
     const double span = vmax > vmin ? vmax - vmin : 1.0;
     for (size_t i = 0; i < size_t(rows) * cols; ++i) out[i] = 0.02 + 0.96 * (out[i] - vmin) / span;
+    return TQSB_OK;
+}
+
+int tqsb_synthetic_image_device(int device, int rows, int cols, uint64_t seed, double* d_out,
+                                void* stream) {
+    if (!d_out || rows < 1 || cols < 1) return set_error(TQSB_EINVAL, "invalid image shape");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+        return set_error(TQSB_ENODEV, "no CUDA device (the library has no CPU fallback)");
+    CUDA_TRY(cudaSetDevice(device));
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int max_parts = 4 * sms;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double* parts = nullptr;
+    CUDA_TRY(cudaMallocAsync(&parts, sizeof(double) * 2 * max_parts, s));
+    const int rc = launch_scene(scene_params(rows, cols, seed), rows, cols, d_out, parts, max_parts,
+                                stream, sms);
+    CUDA_TRY(cudaFreeAsync(parts, s));
+    if (rc != 0) return set_error(TQSB_ECUDA, std::string("scene: ") + cudaGetErrorString(cudaError_t(rc)));
+    return TQSB_OK;
+}
+
+int tqsb_plan_simulate_device(tqsb_plan* p, const double* d_image, int rows, int cols,
+                              double* d_frame, void* stream) {
+    if (!p || !d_image || !d_frame) return set_error(TQSB_EINVAL, "null argument");
+    if (rows < 2 || cols < 2 || rows % 2 != 0 || cols % 2 != 0)
+        return set_error(TQSB_EINVAL, "image dimensions must be even");
+    Device* d = p->devs[0].get();
+    CUDA_TRY(cudaSetDevice(d->id));
+    const int rc = launch_simulate(d_image, rows, cols, d->d_opaque, p->period, d_frame, stream,
+                                   d->num_sms);
+    if (rc != 0)
+        return set_error(TQSB_ECUDA, std::string("simulate: ") + cudaGetErrorString(cudaError_t(rc)));
     return TQSB_OK;
 }
 
@@ -1587,3 +1599,36 @@ int tqsb_probe_peaks(int device, double* fp32_tflops, double* smem_tbps) {
 
 // error reporting shared with io.cpp / tqsk handling (same thread-local message)
 int tqsb_internal_set_error(int code, const std::string& msg) { return set_error(code, msg); }
+
+namespace tqsb {
+// synthetic.cpp:9-30 -- the scene's random parameters, in the reference's draw order
+SceneParams scene_params(int rows, int cols, uint64_t seed) {
+    std::mt19937_64 gen(seed);
+    std::uniform_real_distribution<double> U(0.0, 1.0);
+    const double two_pi = 6.283185307179586;
+    SceneParams sp{};
+    sp.ramp_r = U(gen) * 2.0 - 1.0;
+    sp.ramp_c = U(gen) * 2.0 - 1.0;
+    for (auto& wv : sp.wave) {
+        wv[0] = (U(gen) * 6.0 + 0.5) / rows;
+        wv[1] = (U(gen) * 6.0 + 0.5) / cols;
+        wv[2] = U(gen) * two_pi;
+        wv[3] = U(gen) * 0.5 + 0.1;
+    }
+    const double short_side = std::min(rows, cols);
+    for (auto& bp : sp.bump) {
+        bp[0] = U(gen) * rows;
+        bp[1] = U(gen) * cols;
+        bp[2] = (U(gen) * 0.12 + 0.04) * short_side;
+        bp[3] = (U(gen) * 2.0 - 1.0) * 0.8;
+    }
+    for (auto& ed : sp.edge) {
+        const double theta = U(gen) * two_pi;
+        ed[0] = std::sin(theta);
+        ed[1] = std::cos(theta);
+        ed[2] = U(gen) * (rows + cols) * 0.5;
+        ed[3] = (U(gen) * 2.0 - 1.0) * 0.6;
+    }
+    return sp;
+}
+}  // namespace tqsb

@@ -114,4 +114,19 @@ int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, do
 
 int probe_peaks(int device, double* fp32_tflops, double* smem_tbps);
 
+// synthetic scene parameters (tests/support/synthetic.cpp:9-80), drawn on the host
+struct SceneParams {
+    double ramp_r, ramp_c;
+    double wave[6][4];  // fr, fc, phase, amp
+    double bump[5][4];  // r, c, radius, amp
+    double edge[2][4];  // nr, nc, offset, amp
+};
+SceneParams scene_params(int rows, int cols, uint64_t seed);  // plan.cpp
+
+// sensor.cu: device readout and scene generation (grid-stride, HBM-bound)
+int launch_simulate(const double* d_img, int rows, int cols, const uint8_t* d_opaque, int period,
+                    double* d_frame, void* stream, int num_sms);
+int launch_scene(const SceneParams& sp, int rows, int cols, double* d_out, double* d_parts,
+                 int max_parts, void* stream, int num_sms);
+
 } // namespace tqsb
