@@ -35,6 +35,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 F_BLOCK = 3_723_776  # algorithmic flop per 4x4 block at W=32, nu=200
+# executed: factorised init (~0.2 MFLOP) + 200 x 1024 x 12 flop (update 8, score 4)
+EXEC_FLOP_BLOCK = 200 * 1024 * 12 + 220_000
+NOMINAL_FMA_PER_CLK = 148 * 128  # FP32 lanes of a B200
 METRIC = "megapixels/sec reconstructed (RL-JSDE, 4K frame, period 4x4)"
 
 WORKLOADS = {
@@ -305,6 +308,7 @@ def main_ours(args):
     e2e_value = mp / (e2e_ms * 1e-3)
     kernel_tflops = F_BLOCK * n_blocks / (statistics.mean(step_ms) * 1e-3) / 1e12
 
+    nominal_mhz = (clk or {}).get("sm_max_mhz") or 1965.0
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -348,7 +352,12 @@ def main_ours(args):
                          "algorithmic": f"{F_BLOCK} flop/block x {n_blocks} blocks/launch",
                          "peak_source": "measured this run: FFMA2 probe (tqsb_probe_peaks); "
                                         "MEASURED_PEAKS.json has no FP32 figure",
-                         "smem_tbps_measured": round(peaks["smem_tbps"], 2)},
+                         "smem_tbps_measured": round(peaks["smem_tbps"], 2),
+                         # nominal FP32 pipe: 148 SMs x 128 FMA/clk x 2 flop at the sampled clock
+                         "peak_nominal": round(NOMINAL_FMA_PER_CLK * 2 * nominal_mhz * 1e6 / 1e12, 2),
+                         "frac_nominal": round(kernel_tflops / (NOMINAL_FMA_PER_CLK * 2 * nominal_mhz
+                                                                * 1e6 / 1e12), 4),
+                         "executed_flop_per_block": EXEC_FLOP_BLOCK},
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": int(tot_launch),
