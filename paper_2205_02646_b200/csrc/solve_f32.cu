@@ -33,23 +33,41 @@
 #ifndef TQSB_KEYS
 #define TQSB_KEYS 1  // packed score/position keys (see score_key)
 #endif
-#ifndef TQSB_BRX
-#define TQSB_BRX 0
-#endif
-#ifndef TQSB_WIN
-#define TQSB_WIN 0
-#endif
 #ifndef TQSB_UNI
 #define TQSB_UNI 1
+#endif
+#ifndef TQSB_RELOAD
+#define TQSB_RELOAD 0  // re-read the task after the loop instead of holding it in registers
+#endif
+#ifndef TQSB_TMPICK
+#define TQSB_TMPICK 0  // pick R'_u from a TMEM shadow of the residual (NS == 16)
+#endif
+#ifndef TQSB_LANEREDUX
+#define TQSB_LANEREDUX 0  // owner lane by redux.min instead of ballot + ffs
+#endif
+#ifndef TQSB_TIMING
+#define TQSB_TIMING 0  // per-phase clock() accounting of the iteration (experiment builds)
 #endif
 #ifndef TQSB_AHEAD
 #define TQSB_AHEAD 2  // 4-slot chunks in flight ahead of the update (TQSB_UNI)
 #endif
 
 namespace tqsb {
+#if TQSB_TIMING
+__device__ unsigned long long g_tdbg[16];
+#endif
 namespace {
 
 using namespace dev;
+
+#if TQSB_TIMING
+__device__ __forceinline__ unsigned clk_after(int v) {  // clock read ordered after v is ready
+    unsigned c;
+    asm volatile("{ .reg .pred p; setp.eq.s32 p, %1, -123456789; @p trap; mov.u32 %0, %%clock; }"
+                 : "=r"(c) : "r"(v));
+    return c;
+}
+#endif
 
 // per-warp scratch floats: the init transpose buffer zbuf[gamma][sigma] (float2,
 // row stride 18) / half-spectrum r0buf[sigma][rho], aliased with the element-score
@@ -86,13 +104,17 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
     if (threadIdx.x == 0) s_cls = -1;
     // TMEM tier: a.hot columns x 4*NS TMEM columns per quadrant (512 max)
     const int hotn = a.hot;
-    if (hotn > 0 && warp == 0) {
+    constexpr bool kTmPick = TQSB_TMPICK && NS == 16 && TQSB_KEYS && kWarpsF32 <= 12;
+    const bool tm_alloc = hotn > 0 || kTmPick;
+    if (tm_alloc && warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             static_cast<unsigned>(__cvta_generic_to_shared(&s_tmem))));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tmem_sync_all();
-    const uint32_t tq = hotn > 0 ? s_tmem + (uint32_t(32 * (warp & 3)) << 16) : 0u;
+    const uint32_t tq = tm_alloc ? s_tmem + (uint32_t(32 * (warp & 3)) << 16) : 0u;
+    // residual shadow of this warp: the top 64 x 3 columns of its quadrant (TQSB_TMPICK)
+    [[maybe_unused]] const uint32_t trp = tq + uint32_t(512 - 64 * 3 + 64 * (warp >> 2));
 
     // synthesis pixels of this lane: p = lane + 32 j of the B x B block (loop invariant)
     const int B = a.block;
@@ -201,6 +223,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             __syncwarp();
 #if TQSB_KEYS
             float lmax = score_pass_keys<NS>(R);
+            if constexpr (kTmPick) tmem_st64(trp, R);
 #else
             float lmax = score_pass<NS>(R, srow);
 #endif
@@ -219,8 +242,14 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             const bool tracing = TRACE && ti == 0;
 
             int it = 0;
+#if TQSB_TIMING
+            unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0};
+#endif
             for (; it < a.iterations; ++it) {
                 __syncwarp();
+#if TQSB_TIMING
+                const unsigned t0 = clk_after(__float_as_int(lmax));
+#endif
                 // ---- argmax over the warp (NaN = inadmissible, ignored by max) ----
                 const float gmax = warp_max_f32(lmax);
                 if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
@@ -228,7 +257,17 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 // t through a vector register (a uniform-register switch makes ptxas spill R)
                 int t;
                 asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(31 - int(__float_as_uint(gmax) & 31u)));
+                [[maybe_unused]] float4 rslot;
+                if constexpr (kTmPick) {  // every lane's slot t>>1 of the residual shadow
+                    tmem_wait_st();
+                    rslot = tmem_ld_slot(trp + uint32_t(4 * (t >> 1)));
+                }
+#if TQSB_LANEREDUX
+                int Lw;
+                asm volatile("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(Lw) : "r"(lmax == gmax ? lane : 32));
+#else
                 const int Lw = __ffs(__ballot_sync(FULL, lmax == gmax)) - 1;
+#endif
 #else
                 const unsigned cand = __ballot_sync(FULL, lmax == gmax);
                 int Lw = __ffs(cand) - 1;
@@ -258,10 +297,8 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 const int slot = t >> 1, b = t & 1;
                 const int u = 64 * slot + 2 * Lw + b;
                 // ---- issue the whole C' column now; its latency overlaps the pick ----
-                // windowed column stream (NS == 16, TQSB_WIN): 8 slots ahead
-                constexpr bool kWin = NS == 16 && TQSB_WIN;
                 constexpr bool kUni = NS == 16 && TQSB_UNI;  // one update path for both tiers
-                constexpr int PF = (kWin || kUni) ? 8 : (NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH);
+                constexpr int PF = kUni ? 4 * TQSB_AHEAD : (NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH);
                 float4 c[NS];
                 const float4* col = gcols + size_t(u) * COLF4;
                 const bool in_tmem = u < hotn;
@@ -276,16 +313,6 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 #pragma unroll
                         for (int k = 0; k < 4; ++k) c[4 + k] = t4[k];
                     }
-                } else if constexpr (kWin) {
-                    if (in_tmem) {
-                        float4 t8[PF];
-                        tmem_ld<PF>(tcol, t8);
-#pragma unroll
-                        for (int i = 0; i < PF; ++i) c[i] = t8[i];
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
-                    }
                 } else if (in_tmem) {
                     tmem_ld<NS>(tcol, c);
                 } else {
@@ -293,16 +320,24 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                     for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
                 }
                 const int2 meta = s_meta[u];  // (fac bits, flat k) of rank u
+#if TQSB_TIMING
+                const unsigned t1 = clk_after(u);
+#endif
                 float2 v;
-                if constexpr (NS == 16 && TQSB_BRX)
-                    v = pick_elem_brx(R, t);
-                else
+                if constexpr (kTmPick) {
+                    tmem_wait_ld();
+                    v = (t & 1) ? make_float2(rslot.y, rslot.w) : make_float2(rslot.x, rslot.z);
+                } else {
                     v = pick_elem<NS>(R, t);
+                }
                 const float ure = __shfl_sync(FULL, v.x, Lw);
                 const float uim = __shfl_sync(FULL, v.y, Lw);
                 const float f = __int_as_float(meta.x);
                 const float gre = f * ure, gim = f * uim;
                 const int kflat = meta.y;
+#if TQSB_TIMING
+                const unsigned t2 = clk_after(__float_as_int(gre) ^ __float_as_int(gim));
+#endif
                 // synthesis phases of the kept pixels: issued now, consumed after the update
                 const unsigned sigma = unsigned(kflat) / W, rho = unsigned(kflat) % W;
                 float2 ph[PPL];
@@ -313,11 +348,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 #endif
                 if constexpr (kUni) {
                     lmax = update_uni<NS, TQSB_KEYS, TQSB_AHEAD>(R, c, in_tmem, tcol, col + lane, gre, gim, srow);
-                } else if constexpr (kWin) {
-                    if (in_tmem)
-                        lmax = update_win<NS, PF, true, TQSB_KEYS>(R, c, col, tcol, lane, gre, gim, srow);
-                    else
-                        lmax = update_win<NS, PF, false, TQSB_KEYS>(R, c, col, tcol, lane, gre, gim, srow);
+                    if constexpr (kTmPick) tmem_st64(trp, R);
                 } else {
 #if TQSB_KEYS
                 if (in_tmem) {
@@ -335,6 +366,15 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 }
 #endif
                 }
+#if TQSB_TIMING
+                {
+                    const unsigned t3 = clk_after(__float_as_int(lmax));
+                    tacc[0] += t1 - t0;
+                    tacc[1] += t2 - t1;
+                    tacc[in_tmem ? 2 : 3] += t3 - t2;
+                    tacc[in_tmem ? 4 : 5] += 1;
+                }
+#endif
                 // ---- synthesis of the kept block pixels (off the critical path) ----
 #pragma unroll
                 for (int j = 0; j < PPL; ++j) acc[j] = fmaf(gre, ph[j].x, fmaf(-gim, ph[j].y, acc[j]));
@@ -344,11 +384,27 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                     a.trace_gd[2 * it + 1] = gim;
                 }
             }
+#if TQSB_TIMING
+            if (lane == 0)
+                for (int q = 0; q < 6; ++q) atomicAdd(&g_tdbg[q], tacc[q]);
+#endif
             // ---- placement: clip + crop straight into the output ----
+#if TQSB_RELOAD
+            // (the task and pixel map are re-read here rather than held across the loop)
+            const int2 bo = *reinterpret_cast<const int2*>(a.tasks + ti);
+#else
+            const int2 bo = make_int2(tk.block_row, tk.block_col);
+#endif
 #pragma unroll
             for (int j = 0; j < PPL; ++j) {
-                if (p_r[j] >= 0) {
-                    const int orow = tk.block_row + p_r[j], ocol = tk.block_col + p_c[j];
+#if TQSB_RELOAD
+                const int pj = lane + 32 * j;
+                const int pr = pj < B * B ? pj / B : -1, pcc = pj % B;
+#else
+                const int pr = p_r[j], pcc = p_c[j];
+#endif
+                if (pr >= 0) {
+                    const int orow = bo.x + pr, ocol = bo.y + pcc;
                     if (orow < a.out_rows && ocol < a.out_cols) {
                         float val = acc[j];
                         if (a.clip) val = fminf(fmaxf(val, 0.f), 1.f);
@@ -376,7 +432,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
         }
     }
     tmem_sync_all();
-    if (hotn > 0 && warp == 0)
+    if (tm_alloc && warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem));
 }
 
@@ -411,6 +467,12 @@ int launch_w(const SolveArgs& a, int n_slots, cudaStream_t s, int num_sms) {
 
 } // namespace
 
+#if TQSB_TIMING
+extern "C" int tqsb_debug_timing(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_tdbg, sizeof(unsigned long long) * 6);
+}
+#endif
+
 size_t solve_f32_smem_bytes(int n_slots, int hot) {
     // (fac, perm) per rank + unit table + per-warp scratch; hot columns live in TMEM
     (void)hot;
@@ -420,7 +482,7 @@ size_t solve_f32_smem_bytes(int n_slots, int hot) {
 int solve_f32_max_hot(int n_slots, int device) {
     // TMEM tier: 512 columns per lane quadrant, 4*NS columns per C' column
     (void)device;
-    const int h = 512 / (4 * n_slots);
+    const int h = (TQSB_TMPICK && n_slots == 16 && TQSB_KEYS ? 512 - 64 * 3 : 512) / (4 * n_slots);
     return h < 64 * n_slots ? h : 64 * n_slots;
 }
 
