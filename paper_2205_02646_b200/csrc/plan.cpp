@@ -356,7 +356,9 @@ int device_init(tqsb_plan* p, Device* d) {
     CUDA_TRY(cudaMemcpy(d->d_q64, t.q.data(), sizeof(double) * t.K, cudaMemcpyHostToDevice));
     const int maxhot = solve_f32_max_hot(t.NS, d->id);
     const int K_pad = t.K_pad;
-    int hot = p->cfg.hot_columns < 0 ? maxhot : std::min(p->cfg.hot_columns, maxhot);
+    // auto (-1): no TMEM tier -- with predicated per-chunk loads it costs more issue slots
+    // than it saves (4K frame: 40.6 ms with 8 hot columns vs 40.1 ms without)
+    int hot = p->cfg.hot_columns < 0 ? 0 : std::min(p->cfg.hot_columns, maxhot);
     d->hot = std::clamp(hot, 0, K_pad);
     return TQSB_OK;
 }

@@ -239,7 +239,15 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float4 (&c)[NS]) {
 // (g = column + slot0 * 32 + lane): one code path for both tiers, so the residual
 // registers keep a single allocation. The tcgen05.ld is predicated on a warp-uniform
 // flag; a following tcgen05.wait::ld (unconditional) completes it.
+template <bool TM>
 __device__ __forceinline__ void load_chunk(bool tm, uint32_t taddr, const float4* g, float4 (&d)[4]) {
+    if constexpr (!TM) {  // no TMEM tier: four coalesced 512 B global reads
+        (void)tm;
+        (void)taddr;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[k] = __ldg(g + 32 * k);
+        return;
+    }
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %18, 0;\n\t"
         "@p tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
@@ -257,7 +265,7 @@ __device__ __forceinline__ void load_chunk(bool tm, uint32_t taddr, const float4
 // One update path for both tiers (NS == 16): chunks 0 and 1 (slots 0-7) were issued
 // before the pick; chunk k+2 is issued at the start of chunk k, after the wait::ld
 // that completes chunk k+1.
-template <int NS, bool KEYS, int AHEAD>
+template <int NS, bool KEYS, int AHEAD, bool TM>
 __device__ __forceinline__ float update_uni(float4 (&R)[NS], float4 (&c)[NS], bool tm,
                                             uint32_t taddr, const float4* __restrict__ gl,
                                             float gre, float gim, float* srow) {
@@ -270,11 +278,11 @@ __device__ __forceinline__ float update_uni(float4 (&R)[NS], float4 (&c)[NS], bo
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         if (i % 4 == 0) {
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if constexpr (TM) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             constexpr int A = 4 * AHEAD;  // slots issued ahead of the update
             if (i + A < NS) {
                 float4 t4[4];
-                load_chunk(tm, taddr + uint32_t(4 * (i + A)), gl + (i + A) * 32, t4);
+                load_chunk<TM>(tm, taddr + uint32_t(4 * (i + A)), gl + (i + A) * 32, t4);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) c[i + A + k] = t4[k];
             }

@@ -39,12 +39,6 @@
 #ifndef TQSB_RELOAD
 #define TQSB_RELOAD 0  // re-read the task after the loop instead of holding it in registers
 #endif
-#ifndef TQSB_TMPICK
-#define TQSB_TMPICK 0  // pick R'_u from a TMEM shadow of the residual (NS == 16)
-#endif
-#ifndef TQSB_LANEREDUX
-#define TQSB_LANEREDUX 0  // owner lane by redux.min instead of ballot + ffs
-#endif
 #ifndef TQSB_TIMING
 #define TQSB_TIMING 0  // per-phase clock() accounting of the iteration (experiment builds)
 #endif
@@ -80,7 +74,7 @@ struct Scratch {
     static constexpr int kFloats = (kZ > kR ? (kZ > kS ? kZ : kS) : (kR > kS ? kR : kS));
 };
 
-template <int NS, int W, int PPL, bool TRACE>
+template <int NS, int W, int PPL, bool TRACE, bool TM>
 __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs a) {
     extern __shared__ __align__(16) float smem[];
     constexpr int COLF4 = NS * 32;  // float4 per column
@@ -103,9 +97,8 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
     for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].y = a.wc.perm[r];
     if (threadIdx.x == 0) s_cls = -1;
     // TMEM tier: a.hot columns x 4*NS TMEM columns per quadrant (512 max)
-    const int hotn = a.hot;
-    constexpr bool kTmPick = TQSB_TMPICK && NS == 16 && TQSB_KEYS && kWarpsF32 <= 12;
-    const bool tm_alloc = hotn > 0 || kTmPick;
+    const int hotn = TM ? a.hot : 0;  // TMEM tier (TM instantiations only)
+    const bool tm_alloc = hotn > 0;
     if (tm_alloc && warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             static_cast<unsigned>(__cvta_generic_to_shared(&s_tmem))));
@@ -113,8 +106,6 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
     }
     tmem_sync_all();
     const uint32_t tq = tm_alloc ? s_tmem + (uint32_t(32 * (warp & 3)) << 16) : 0u;
-    // residual shadow of this warp: the top 64 x 3 columns of its quadrant (TQSB_TMPICK)
-    [[maybe_unused]] const uint32_t trp = tq + uint32_t(512 - 64 * 3 + 64 * (warp >> 2));
 
     // synthesis pixels of this lane: p = lane + 32 j of the B x B block (loop invariant)
     const int B = a.block;
@@ -223,7 +214,6 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             __syncwarp();
 #if TQSB_KEYS
             float lmax = score_pass_keys<NS>(R);
-            if constexpr (kTmPick) tmem_st64(trp, R);
 #else
             float lmax = score_pass<NS>(R, srow);
 #endif
@@ -257,17 +247,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 // t through a vector register (a uniform-register switch makes ptxas spill R)
                 int t;
                 asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(31 - int(__float_as_uint(gmax) & 31u)));
-                [[maybe_unused]] float4 rslot;
-                if constexpr (kTmPick) {  // every lane's slot t>>1 of the residual shadow
-                    tmem_wait_st();
-                    rslot = tmem_ld_slot(trp + uint32_t(4 * (t >> 1)));
-                }
-#if TQSB_LANEREDUX
-                int Lw;
-                asm volatile("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(Lw) : "r"(lmax == gmax ? lane : 32));
-#else
                 const int Lw = __ffs(__ballot_sync(FULL, lmax == gmax)) - 1;
-#endif
 #else
                 const unsigned cand = __ballot_sync(FULL, lmax == gmax);
                 int Lw = __ffs(cand) - 1;
@@ -301,15 +281,15 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 constexpr int PF = kUni ? 4 * TQSB_AHEAD : (NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH);
                 float4 c[NS];
                 const float4* col = gcols + size_t(u) * COLF4;
-                const bool in_tmem = u < hotn;
+                const bool in_tmem = TM && u < hotn;
                 const uint32_t tcol = tq + uint32_t(u * 4 * NS);
                 if constexpr (kUni) {
                     float4 t4[4];
-                    load_chunk(in_tmem, tcol, col + lane, t4);
+                    load_chunk<TM>(in_tmem, tcol, col + lane, t4);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) c[k] = t4[k];
                     if constexpr (TQSB_AHEAD > 1) {
-                        load_chunk(in_tmem, tcol + 16u, col + 4 * 32 + lane, t4);
+                        load_chunk<TM>(in_tmem, tcol + 16u, col + 4 * 32 + lane, t4);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) c[4 + k] = t4[k];
                     }
@@ -323,13 +303,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 #if TQSB_TIMING
                 const unsigned t1 = clk_after(u);
 #endif
-                float2 v;
-                if constexpr (kTmPick) {
-                    tmem_wait_ld();
-                    v = (t & 1) ? make_float2(rslot.y, rslot.w) : make_float2(rslot.x, rslot.z);
-                } else {
-                    v = pick_elem<NS>(R, t);
-                }
+                const float2 v = pick_elem<NS>(R, t);
                 const float ure = __shfl_sync(FULL, v.x, Lw);
                 const float uim = __shfl_sync(FULL, v.y, Lw);
                 const float f = __int_as_float(meta.x);
@@ -347,8 +321,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
                 __syncwarp();  // all score reads of this iteration precede the rewrite
 #endif
                 if constexpr (kUni) {
-                    lmax = update_uni<NS, TQSB_KEYS, TQSB_AHEAD>(R, c, in_tmem, tcol, col + lane, gre, gim, srow);
-                    if constexpr (kTmPick) tmem_st64(trp, R);
+                    lmax = update_uni<NS, TQSB_KEYS, TQSB_AHEAD, TM>(R, c, in_tmem, tcol, col + lane, gre, gim, srow);
                 } else {
 #if TQSB_KEYS
                 if (in_tmem) {
@@ -439,7 +412,11 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 template <int NS, int W, int PPL>
 int launch_one(const SolveArgs& a, cudaStream_t stream, int num_sms) {
     const size_t smem = solve_f32_smem_bytes(NS, a.hot) ;
-    auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true> : k_solve_f32<NS, W, PPL, false>;
+    // the TMEM column tier only when columns are assigned to it (results are identical
+    // either way; it costs instructions: measured 40.6 vs 40.1 ms per 4K frame with it on)
+    auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true, false>
+                : a.hot > 0   ? k_solve_f32<NS, W, PPL, false, true>
+                              : k_solve_f32<NS, W, PPL, false, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
@@ -482,7 +459,7 @@ size_t solve_f32_smem_bytes(int n_slots, int hot) {
 int solve_f32_max_hot(int n_slots, int device) {
     // TMEM tier: 512 columns per lane quadrant, 4*NS columns per C' column
     (void)device;
-    const int h = (TQSB_TMPICK && n_slots == 16 && TQSB_KEYS ? 512 - 64 * 3 : 512) / (4 * n_slots);
+    const int h = 512 / (4 * n_slots);
     return h < 64 * n_slots ? h : 64 * n_slots;
 }
 

@@ -71,3 +71,16 @@ def test_4k_properties(tq, need_gpu, frame_4k):
         torch.cuda.synchronize()
         assert d_out.cpu().numpy().tobytes() == a.tobytes()
     assert np.all((a >= 0) & (a <= 1))
+
+
+def test_tmem_tier_is_result_neutral(tq, need_gpu):
+    """The TMEM column tier (hot_columns > 0) only changes where C' columns are read
+    from: outputs are bitwise identical with and without it."""
+    gt = tq.synthetic_image(512, 512, 402)
+    pat = tq.generate_pattern(7, 8)
+    frame = tq.simulate_measurement(gt, pat)
+    outs = []
+    for hot in (0, 4, 8):
+        with tq.Plan(pat, tq.ReconstructionConfig(hot_columns=hot)) as plan:
+            outs.append(plan.reconstruct(frame).output)
+    assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
