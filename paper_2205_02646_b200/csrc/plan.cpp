@@ -272,6 +272,7 @@ struct WorkKey {
 struct Work {
     Task* d_tasks = nullptr;
     WorkItem* d_items = nullptr;
+    int* d_task_cls = nullptr;       // class slot per (class-sorted) task
     int n_tasks = 0, n_items = 0;
     int frame_row0 = 0, frame_row1 = 0;  // frame rows the band needs
     std::vector<int> keys;                // classes used
@@ -292,6 +293,7 @@ struct Device {
     double* d_unit64 = nullptr;
     double* d_q64 = nullptr;
     uint8_t* d_opaque = nullptr;   // the pattern's (P/2)^2 quadrant indices (device readout)
+    int* d_counter = nullptr;      // dynamic task queue head of the fp32 solve
     std::map<int, int> slot_of;    // class key -> slot
     std::vector<ClassTab> tabs;    // host mirror
     std::vector<ClassSlab> slabs;
@@ -348,6 +350,7 @@ int device_init(tqsb_plan* p, Device* d) {
     CUDA_TRY(cudaMalloc(&d->d_unit64, sizeof(double) * 2 * t.W));
     CUDA_TRY(cudaMalloc(&d->d_q64, sizeof(double) * t.K));
     CUDA_TRY(cudaMalloc(&d->d_opaque, p->opaque.size()));
+    CUDA_TRY(cudaMalloc(&d->d_counter, sizeof(int)));
     CUDA_TRY(cudaMemcpy(d->d_opaque, p->opaque.data(), p->opaque.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_perm, t.perm.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_src, t.src.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
@@ -370,6 +373,7 @@ void device_free(Device* d) {
     for (auto& kv : d->works) {
         cudaFree(kv.second.d_tasks);
         cudaFree(kv.second.d_items);
+        cudaFree(kv.second.d_task_cls);
     }
     cudaFree(d->d_tabs);
     cudaFree(d->d_perm);
@@ -378,6 +382,7 @@ void device_free(Device* d) {
     cudaFree(d->d_unit64);
     cudaFree(d->d_q64);
     cudaFree(d->d_opaque);
+    cudaFree(d->d_counter);
     cudaFree(d->d_frame);
     cudaFree(d->d_out);
     if (d->h_in) cudaFreeHost(d->h_in);
@@ -553,7 +558,9 @@ int prepare_band(tqsb_plan* p, Device* d, const Geometry& g, int frame_rows, int
     for (size_t i = 0; i < e.tasks.size(); ++i) by_key[e.keys[i]].push_back(e.tasks[i]);
     std::vector<Task> sorted;
     std::vector<WorkItem> items;
+    std::vector<int> task_cls;
     sorted.reserve(e.tasks.size());
+    task_cls.reserve(e.tasks.size());
     const int chunk = (p->cfg.compute == TQSB_COMPUTE_FP32 ? kWarpsF32 : kWarpsF64) * 4;
     for (int k : e.class_order) {
         const auto& v = by_key[k];
@@ -565,6 +572,7 @@ int prepare_band(tqsb_plan* p, Device* d, const Geometry& g, int frame_rows, int
             items.push_back(wi);
         }
         sorted.insert(sorted.end(), v.begin(), v.end());
+        task_cls.insert(task_cls.end(), v.size(), d->slot_of.at(k));
     }
     w.n_items = int(items.size());
     (void)frame_cols;
@@ -574,6 +582,9 @@ int prepare_band(tqsb_plan* p, Device* d, const Geometry& g, int frame_rows, int
     CUDA_TRY(cudaMemcpy(w.d_tasks, sorted.data(), sizeof(Task) * sorted.size(),
                         cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(w.d_items, items.data(), sizeof(WorkItem) * items.size(),
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&w.d_task_cls, sizeof(int) * std::max<size_t>(1, task_cls.size())));
+    CUDA_TRY(cudaMemcpy(w.d_task_cls, task_cls.data(), sizeof(int) * task_cls.size(),
                         cudaMemcpyHostToDevice));
     auto ins = d->works.emplace(wkey, std::move(w));
     *out = &ins.first->second;
@@ -626,10 +637,12 @@ SolveArgs base_args(tqsb_plan* p, Device* d) {
     a.hot = d->hot;
     a.early_stop = p->cfg.early_stop;
     a.early_stop_scale = p->cfg.early_stop_scale;
+    a.counter = d->d_counter;
     return a;
 }
 
 int launch(tqsb_plan* p, Device* d, const SolveArgs& a, cudaStream_t s) {
+    if (a.counter) CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
     int rc = p->cfg.algorithm == TQSB_ALGO_LJSDE ? launch_solve_ljsde(a, s, d->num_sms)
              : p->cfg.compute == TQSB_COMPUTE_FP32 ? launch_solve_f32(a, p->wt.NS, s, d->num_sms)
                                                    : launch_solve_f64(a, s, d->num_sms);
@@ -704,6 +717,8 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
     a.tasks = w->d_tasks;
     a.items = w->d_items;
     a.n_items = w->n_items;
+    a.task_cls = w->d_task_cls;
+    a.n_tasks = w->n_tasks;
     cudaEventRecord(d->ev0, d->stream);
     if (w->n_items > 0) {
         if ((rc = launch(p, d, a, d->stream))) return fail(rc);
@@ -784,6 +799,8 @@ void run_batch_host(tqsb_plan* p, Device* d, const Geometry& g, const double* co
         a.tasks = w->d_tasks;
         a.items = w->d_items;
         a.n_items = w->n_items;
+        a.task_cls = w->d_task_cls;
+        a.n_tasks = w->n_tasks;
         if (i == 0) cudaEventRecord(d->ev0, d->stream);
         if (w->n_items > 0) {
             if ((rc = launch(p, d, a, d->stream))) return fail(rc);
@@ -1093,6 +1110,8 @@ static int device_band(tqsb_plan* p, const double* d_frame, int frame_rows, int 
     a.tasks = w->d_tasks;
     a.items = w->d_items;
     a.n_items = w->n_items;
+    a.task_cls = w->d_task_cls;
+    a.n_tasks = w->n_tasks;
     if (w->n_items > 0) {
         TQSB_TRY(launch(p, d, a, static_cast<cudaStream_t>(stream)));
         launches += 1;

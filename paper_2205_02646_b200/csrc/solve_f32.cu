@@ -39,6 +39,9 @@
 #ifndef TQSB_RELOAD
 #define TQSB_RELOAD 0  // re-read the task after the loop instead of holding it in registers
 #endif
+#ifndef TQSB_DYN
+#define TQSB_DYN 1  // warp-level dynamic task scheduling when no CTA-wide class state is needed
+#endif
 #ifndef TQSB_TIMING
 #define TQSB_TIMING 0  // per-phase clock() accounting of the iteration (experiment builds)
 #endif
@@ -76,6 +79,7 @@ struct Scratch {
 
 template <int NS, int W, int PPL, bool TRACE, bool TM>
 __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs a) {
+    constexpr bool DYN = !TRACE && !TM && TQSB_DYN;  // per-warp task queue (a.counter)
     extern __shared__ __align__(16) float smem[];
     constexpr int COLF4 = NS * 32;  // float4 per column
     constexpr int KP = NS * 64;     // padded frequency count
@@ -118,290 +122,309 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
         p_c[j] = p < nb2 ? p % B : 0;
     }
 
-    for (int it_item = blockIdx.x; it_item < a.n_items; it_item += gridDim.x) {
-        const WorkItem item = a.items[it_item];
-        if (item.cls != s_cls) {  // CTA-uniform: refill the class's on-chip tables
-            tmem_sync_all();
-            const float4* src = reinterpret_cast<const float4*>(a.tabs[item.cls].cpack);
-            if (warp < 4) {  // one warp per TMEM lane quadrant copies the hot columns
-                for (int j = 0; j < hotn; ++j) {
-#pragma unroll
-                    for (int i = 0; i < NS; ++i)
-                        tmem_st4(tq + uint32_t(j * 4 * NS + 4 * i), __ldg(src + size_t(j) * COLF4 + i * 32 + lane));
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            }
-            const float* fsrc = a.tabs[item.cls].fac;
-            for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].x = __float_as_int(__ldg(fsrc + r));
-            tmem_sync_all();
-            if (threadIdx.x == 0) s_cls = item.cls;
-            __syncthreads();
-        }
-        const ClassTab ct = a.tabs[item.cls];
+    // one target block end to end: init, nu iterations, synthesis, placement
+    auto solve_task = [&](const int ti, const ClassTab& ct) {
         const float4* __restrict__ gcols = reinterpret_cast<const float4*>(ct.cpack);
         const float2* __restrict__ scale2 = reinterpret_cast<const float2*>(ct.scale);
-
-        for (int ti = item.start + warp; ti < item.start + item.count; ti += kWarpsF32) {
-            const Task tk = a.tasks[ti];
-            // ---------------- init: window image column per lane ----------------
-            float colv[W];
-            {
-                int fc = (tk.origin_col + lane) >> 1;
-                fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
+        const Task tk = a.tasks[ti];
+        // ---------------- init: window image column per lane ----------------
+        float colv[W];
+        {
+            int fc = (tk.origin_col + lane) >> 1;
+            fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
 #pragma unroll
-                for (int eta = 0; eta < W; ++eta) {
-                    float v = 0.f;
-                    if (lane < W) {
-                        const float mk = __ldg(ct.mask32 + eta * W + lane);
-                        int fr = (tk.origin_row + eta) >> 1;
-                        fr = fr < a.frame_rows - 1 ? fr : a.frame_rows - 1;
-                        const double y =
-                            __ldg(a.frame + size_t(fr - a.frame_row0) * a.frame_pitch + fc);
-                        v = mk * float(y);
-                    }
-                    colv[eta] = v;
+            for (int eta = 0; eta < W; ++eta) {
+                float v = 0.f;
+                if (lane < W) {
+                    const float mk = __ldg(ct.mask32 + eta * W + lane);
+                    int fr = (tk.origin_row + eta) >> 1;
+                    fr = fr < a.frame_rows - 1 ? fr : a.frame_rows - 1;
+                    const double y =
+                        __ldg(a.frame + size_t(fr - a.frame_row0) * a.frame_pitch + fc);
+                    v = mk * float(y);
                 }
+                colv[eta] = v;
             }
-            // step 1 (lane = gamma): Z(sigma, gamma) = sum_eta a(eta,gamma) conj(U(eta sigma))
-            constexpr int H = W / 2 + 1;
+        }
+        // step 1 (lane = gamma): Z(sigma, gamma) = sum_eta a(eta,gamma) conj(U(eta sigma))
+        constexpr int H = W / 2 + 1;
+#pragma unroll
+        for (int sg = 0; sg < H; ++sg) {
+            float zr = 0.f, zi = 0.f;
+#pragma unroll
+            for (int eta = 0; eta < W; ++eta) {
+                const float2 u = unit[(eta * sg) % W];
+                zr = fmaf(colv[eta], u.x, zr);
+                zi = fmaf(-colv[eta], u.y, zi);
+            }
+            zbuf[lane * 18 + sg] = make_float2(zr, zi);
+        }
+        __syncwarp();
+        // step 2 (lane = rho): R0(sigma, rho) = sum_gamma Z(sigma,gamma) conj(U(gamma rho))
+        float2 r0[H];
+#pragma unroll
+        for (int sg = 0; sg < H; ++sg) r0[sg] = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int g = 0; g < W; ++g) {
+            const float2 u = unit[(g * lane) % W];
 #pragma unroll
             for (int sg = 0; sg < H; ++sg) {
-                float zr = 0.f, zi = 0.f;
-#pragma unroll
-                for (int eta = 0; eta < W; ++eta) {
-                    const float2 u = unit[(eta * sg) % W];
-                    zr = fmaf(colv[eta], u.x, zr);
-                    zi = fmaf(-colv[eta], u.y, zi);
-                }
-                zbuf[lane * 18 + sg] = make_float2(zr, zi);
+                const float2 z = zbuf[g * 18 + sg];
+                r0[sg].x = fmaf(z.x, u.x, fmaf(z.y, u.y, r0[sg].x));
+                r0[sg].y = fmaf(z.y, u.x, fmaf(-z.x, u.y, r0[sg].y));
             }
-            __syncwarp();
-            // step 2 (lane = rho): R0(sigma, rho) = sum_gamma Z(sigma,gamma) conj(U(gamma rho))
-            float2 r0[H];
+        }
+        __syncwarp();
+        float2* r0buf = zbuf;
+        if (lane < W) {
 #pragma unroll
-            for (int sg = 0; sg < H; ++sg) r0[sg] = make_float2(0.f, 0.f);
-#pragma unroll 4
-            for (int g = 0; g < W; ++g) {
-                const float2 u = unit[(g * lane) % W];
+            for (int sg = 0; sg < H; ++sg) r0buf[sg * W + lane] = r0[sg];
+        }
+        __syncwarp();
+        // gather into rank order and scale: R'_r = s_r R0[perm r]
+        float4 R[NS];
 #pragma unroll
-                for (int sg = 0; sg < H; ++sg) {
-                    const float2 z = zbuf[g * 18 + sg];
-                    r0[sg].x = fmaf(z.x, u.x, fmaf(z.y, u.y, r0[sg].x));
-                    r0[sg].y = fmaf(z.y, u.x, fmaf(-z.x, u.y, r0[sg].y));
-                }
-            }
-            __syncwarp();
-            float2* r0buf = zbuf;
-            if (lane < W) {
-#pragma unroll
-                for (int sg = 0; sg < H; ++sg) r0buf[sg * W + lane] = r0[sg];
-            }
-            __syncwarp();
-            // gather into rank order and scale: R'_r = s_r R0[perm r]
-            float4 R[NS];
-#pragma unroll
-            for (int i = 0; i < NS; ++i) {
-                const int r = 64 * i + 2 * lane;
-                const int s0 = __ldg(a.wc.src + r), s1 = __ldg(a.wc.src + r + 1);
-                const float2 sc = __ldg(scale2 + 32 * i + lane);
-                float2 v0 = r0buf[s0 & 0xffff], v1 = r0buf[s1 & 0xffff];
-                if (s0 & (1 << 30)) v0.y = -v0.y;
-                if (s1 & (1 << 30)) v1.y = -v1.y;
-                const float2 re = __fmul2_rn(sc, make_float2(v0.x, v1.x));
-                const float2 im = __fmul2_rn(sc, make_float2(v0.y, v1.y));
-                R[i] = make_float4(re.x, re.y, im.x, im.y);
-            }
-            __syncwarp();
+        for (int i = 0; i < NS; ++i) {
+            const int r = 64 * i + 2 * lane;
+            const int s0 = __ldg(a.wc.src + r), s1 = __ldg(a.wc.src + r + 1);
+            const float2 sc = __ldg(scale2 + 32 * i + lane);
+            float2 v0 = r0buf[s0 & 0xffff], v1 = r0buf[s1 & 0xffff];
+            if (s0 & (1 << 30)) v0.y = -v0.y;
+            if (s1 & (1 << 30)) v1.y = -v1.y;
+            const float2 re = __fmul2_rn(sc, make_float2(v0.x, v1.x));
+            const float2 im = __fmul2_rn(sc, make_float2(v0.y, v1.y));
+            R[i] = make_float4(re.x, re.y, im.x, im.y);
+        }
+        __syncwarp();
 #if TQSB_KEYS
-            float lmax = score_pass_keys<NS>(R);
+        float lmax = score_pass_keys<NS>(R);
 #else
-            float lmax = score_pass<NS>(R, srow);
+        float lmax = score_pass<NS>(R, srow);
 #endif
 
-            float acc[PPL];
+        float acc[PPL];
 #pragma unroll
-            for (int j = 0; j < PPL; ++j) acc[j] = 0.f;
-            const int rw = tk.block_row - tk.origin_row, cw = tk.block_col - tk.origin_col;
-            // window coordinates of this lane's kept pixels (unsigned: cheap mod W)
-            unsigned pe[PPL], pg[PPL];
+        for (int j = 0; j < PPL; ++j) acc[j] = 0.f;
+        const int rw = tk.block_row - tk.origin_row, cw = tk.block_col - tk.origin_col;
+        // window coordinates of this lane's kept pixels (unsigned: cheap mod W)
+        unsigned pe[PPL], pg[PPL];
 #pragma unroll
-            for (int j = 0; j < PPL; ++j) {
-                pe[j] = unsigned(rw + (p_r[j] < 0 ? 0 : p_r[j]));
-                pg[j] = unsigned(cw + p_c[j]);
-            }
-            const bool tracing = TRACE && ti == 0;
+        for (int j = 0; j < PPL; ++j) {
+            pe[j] = unsigned(rw + (p_r[j] < 0 ? 0 : p_r[j]));
+            pg[j] = unsigned(cw + p_c[j]);
+        }
+        const bool tracing = TRACE && ti == 0;
 
-            int it = 0;
+        int it = 0;
 #if TQSB_TIMING
-            unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0};
+        unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0};
 #endif
-            for (; it < a.iterations; ++it) {
-                __syncwarp();
+        for (; it < a.iterations; ++it) {
+            __syncwarp();
 #if TQSB_TIMING
-                const unsigned t0 = clk_after(__float_as_int(lmax));
+            const unsigned t0 = clk_after(__float_as_int(lmax));
 #endif
-                // ---- argmax over the warp (NaN = inadmissible, ignored by max) ----
-                const float gmax = warp_max_f32(lmax);
-                if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
+            // ---- argmax over the warp (NaN = inadmissible, ignored by max) ----
+            const float gmax = warp_max_f32(lmax);
+            if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
 #if TQSB_KEYS
-                // t through a vector register (a uniform-register switch makes ptxas spill R)
-                int t;
-                asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(31 - int(__float_as_uint(gmax) & 31u)));
-                const int Lw = __ffs(__ballot_sync(FULL, lmax == gmax)) - 1;
+            // t through a vector register (a uniform-register switch makes ptxas spill R)
+            int t;
+            asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(31 - int(__float_as_uint(gmax) & 31u)));
+            const int Lw = __ffs(__ballot_sync(FULL, lmax == gmax)) - 1;
 #else
-                const unsigned cand = __ballot_sync(FULL, lmax == gmax);
-                int Lw = __ffs(cand) - 1;
-                const float sv = lane < 2 * NS ? scr[Lw * kSbufStride + lane] : qnan();
-                const unsigned hit = __ballot_sync(FULL, sv == gmax);
-                int t;  // element index within lane Lw: slot t>>1, half t&1
-                if (__popc(cand) == 1 && __popc(hit) == 1) {
-                    t = __ffs(hit) - 1;
-                } else {
-                    // ties: smallest flat index among all maxima (rljsde.cpp:147-156)
-                    unsigned key = 0xffffffffu;
+            const unsigned cand = __ballot_sync(FULL, lmax == gmax);
+            int Lw = __ffs(cand) - 1;
+            const float sv = lane < 2 * NS ? scr[Lw * kSbufStride + lane] : qnan();
+            const unsigned hit = __ballot_sync(FULL, sv == gmax);
+            int t;  // element index within lane Lw: slot t>>1, half t&1
+            if (__popc(cand) == 1 && __popc(hit) == 1) {
+                t = __ffs(hit) - 1;
+            } else {
+                // ties: smallest flat index among all maxima (rljsde.cpp:147-156)
+                unsigned key = 0xffffffffu;
 #pragma unroll
-                    for (int e = 0; e < 2 * NS; ++e) {
-                        if (srow[e] == gmax) {
-                            const int r = 64 * (e >> 1) + 2 * lane + (e & 1);
-                            key = min(key, (unsigned(s_meta[r].y) << 16) | unsigned(r));
-                        }
+                for (int e = 0; e < 2 * NS; ++e) {
+                    if (srow[e] == gmax) {
+                        const int r = 64 * (e >> 1) + 2 * lane + (e & 1);
+                        key = min(key, (unsigned(s_meta[r].y) << 16) | unsigned(r));
                     }
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1)
-                        key = min(key, __shfl_xor_sync(FULL, key, off));
-                    const int r = int(key & 0xffffu);
-                    Lw = (r >> 1) & 31;
-                    t = 2 * (r >> 6) + (r & 1);
                 }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1)
+                    key = min(key, __shfl_xor_sync(FULL, key, off));
+                const int r = int(key & 0xffffu);
+                Lw = (r >> 1) & 31;
+                t = 2 * (r >> 6) + (r & 1);
+            }
 #endif
-                const int slot = t >> 1, b = t & 1;
-                const int u = 64 * slot + 2 * Lw + b;
-                // ---- issue the whole C' column now; its latency overlaps the pick ----
-                constexpr bool kUni = NS == 16 && TQSB_UNI;  // one update path for both tiers
-                constexpr int PF = kUni ? 4 * TQSB_AHEAD : (NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH);
-                float4 c[NS];
-                const float4* col = gcols + size_t(u) * COLF4;
-                const bool in_tmem = TM && u < hotn;
-                const uint32_t tcol = tq + uint32_t(u * 4 * NS);
-                if constexpr (kUni) {
-                    float4 t4[4];
-                    load_chunk<TM>(in_tmem, tcol, col + lane, t4);
+            const int slot = t >> 1, b = t & 1;
+            const int u = 64 * slot + 2 * Lw + b;
+            // ---- issue the whole C' column now; its latency overlaps the pick ----
+            constexpr bool kUni = NS == 16 && TQSB_UNI;  // one update path for both tiers
+            constexpr int PF = kUni ? 4 * TQSB_AHEAD : (NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH);
+            float4 c[NS];
+            const float4* col = gcols + size_t(u) * COLF4;
+            const bool in_tmem = TM && u < hotn;
+            const uint32_t tcol = tq + uint32_t(u * 4 * NS);
+            if constexpr (kUni) {
+                float4 t4[4];
+                load_chunk<TM>(in_tmem, tcol, col + lane, t4);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) c[k] = t4[k];
-                    if constexpr (TQSB_AHEAD > 1) {
-                        load_chunk<TM>(in_tmem, tcol + 16u, col + 4 * 32 + lane, t4);
+                for (int k = 0; k < 4; ++k) c[k] = t4[k];
+                if constexpr (TQSB_AHEAD > 1) {
+                    load_chunk<TM>(in_tmem, tcol + 16u, col + 4 * 32 + lane, t4);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) c[4 + k] = t4[k];
-                    }
-                } else if (in_tmem) {
-                    tmem_ld<NS>(tcol, c);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
+                    for (int k = 0; k < 4; ++k) c[4 + k] = t4[k];
                 }
-                const int2 meta = s_meta[u];  // (fac bits, flat k) of rank u
-#if TQSB_TIMING
-                const unsigned t1 = clk_after(u);
-#endif
-                const float2 v = pick_elem<NS>(R, t);
-                const float ure = __shfl_sync(FULL, v.x, Lw);
-                const float uim = __shfl_sync(FULL, v.y, Lw);
-                const float f = __int_as_float(meta.x);
-                const float gre = f * ure, gim = f * uim;
-                const int kflat = meta.y;
-#if TQSB_TIMING
-                const unsigned t2 = clk_after(__float_as_int(gre) ^ __float_as_int(gim));
-#endif
-                // synthesis phases of the kept pixels: issued now, consumed after the update
-                const unsigned sigma = unsigned(kflat) / W, rho = unsigned(kflat) % W;
-                float2 ph[PPL];
+            } else if (in_tmem) {
+                tmem_ld<NS>(tcol, c);
+            } else {
 #pragma unroll
-                for (int j = 0; j < PPL; ++j) ph[j] = unit[(pe[j] * sigma + pg[j] * rho) % unsigned(W)];
+                for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
+            }
+            // (fac bits, flat k) of rank u: CTA-shared table, or through L1 when scheduled per warp
+            const int2 meta = DYN ? make_int2(__float_as_int(__ldg(ct.fac + u)), __ldg(a.wc.perm + u))
+                                  : s_meta[u];
+#if TQSB_TIMING
+            const unsigned t1 = clk_after(u);
+#endif
+            const float2 v = pick_elem<NS>(R, t);
+            const float ure = __shfl_sync(FULL, v.x, Lw);
+            const float uim = __shfl_sync(FULL, v.y, Lw);
+            const float f = __int_as_float(meta.x);
+            const float gre = f * ure, gim = f * uim;
+            const int kflat = meta.y;
+#if TQSB_TIMING
+            const unsigned t2 = clk_after(__float_as_int(gre) ^ __float_as_int(gim));
+#endif
+            // synthesis phases of the kept pixels: issued now, consumed after the update
+            const unsigned sigma = unsigned(kflat) / W, rho = unsigned(kflat) % W;
+            float2 ph[PPL];
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) ph[j] = unit[(pe[j] * sigma + pg[j] * rho) % unsigned(W)];
 #if !TQSB_KEYS
-                __syncwarp();  // all score reads of this iteration precede the rewrite
+            __syncwarp();  // all score reads of this iteration precede the rewrite
 #endif
-                if constexpr (kUni) {
-                    lmax = update_uni<NS, TQSB_KEYS, TQSB_AHEAD, TM>(R, c, in_tmem, tcol, col + lane, gre, gim, srow);
-                } else {
+            if constexpr (kUni) {
+                lmax = update_uni<NS, TQSB_KEYS, TQSB_AHEAD, TM>(R, c, in_tmem, tcol, col + lane, gre, gim, srow);
+            } else {
 #if TQSB_KEYS
-                if (in_tmem) {
-                    tmem_wait_ld();
-                    lmax = update_pass_keys<NS, NS>(R, c, col, lane, gre, gim);
-                } else {
-                    lmax = update_pass_keys<NS, PF>(R, c, col, lane, gre, gim);
-                }
+            if (in_tmem) {
+                tmem_wait_ld();
+                lmax = update_pass_keys<NS, NS>(R, c, col, lane, gre, gim);
+            } else {
+                lmax = update_pass_keys<NS, PF>(R, c, col, lane, gre, gim);
+            }
 #else
-                if (in_tmem) {
-                    tmem_wait_ld();
-                    lmax = update_pass<NS, NS>(R, c, col, lane, gre, gim, srow);
-                } else {
-                    lmax = update_pass<NS, PF>(R, c, col, lane, gre, gim, srow);
-                }
+            if (in_tmem) {
+                tmem_wait_ld();
+                lmax = update_pass<NS, NS>(R, c, col, lane, gre, gim, srow);
+            } else {
+                lmax = update_pass<NS, PF>(R, c, col, lane, gre, gim, srow);
+            }
 #endif
-                }
-#if TQSB_TIMING
-                {
-                    const unsigned t3 = clk_after(__float_as_int(lmax));
-                    tacc[0] += t1 - t0;
-                    tacc[1] += t2 - t1;
-                    tacc[in_tmem ? 2 : 3] += t3 - t2;
-                    tacc[in_tmem ? 4 : 5] += 1;
-                }
-#endif
-                // ---- synthesis of the kept block pixels (off the critical path) ----
-#pragma unroll
-                for (int j = 0; j < PPL; ++j) acc[j] = fmaf(gre, ph[j].x, fmaf(-gim, ph[j].y, acc[j]));
-                if (tracing && lane == 0) {
-                    a.trace_picks[it] = kflat;
-                    a.trace_gd[2 * it] = gre;
-                    a.trace_gd[2 * it + 1] = gim;
-                }
             }
 #if TQSB_TIMING
-            if (lane == 0)
-                for (int q = 0; q < 6; ++q) atomicAdd(&g_tdbg[q], tacc[q]);
+            {
+                const unsigned t3 = clk_after(__float_as_int(lmax));
+                tacc[0] += t1 - t0;
+                tacc[1] += t2 - t1;
+                tacc[in_tmem ? 2 : 3] += t3 - t2;
+                tacc[in_tmem ? 4 : 5] += 1;
+            }
 #endif
-            // ---- placement: clip + crop straight into the output ----
+            // ---- synthesis of the kept block pixels (off the critical path) ----
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) acc[j] = fmaf(gre, ph[j].x, fmaf(-gim, ph[j].y, acc[j]));
+            if (tracing && lane == 0) {
+                a.trace_picks[it] = kflat;
+                a.trace_gd[2 * it] = gre;
+                a.trace_gd[2 * it + 1] = gim;
+            }
+        }
+#if TQSB_TIMING
+        if (lane == 0)
+            for (int q = 0; q < 6; ++q) atomicAdd(&g_tdbg[q], tacc[q]);
+#endif
+        // ---- placement: clip + crop straight into the output ----
 #if TQSB_RELOAD
-            // (the task and pixel map are re-read here rather than held across the loop)
-            const int2 bo = *reinterpret_cast<const int2*>(a.tasks + ti);
+        // (the task and pixel map are re-read here rather than held across the loop)
+        const int2 bo = *reinterpret_cast<const int2*>(a.tasks + ti);
 #else
-            const int2 bo = make_int2(tk.block_row, tk.block_col);
+        const int2 bo = make_int2(tk.block_row, tk.block_col);
 #endif
 #pragma unroll
-            for (int j = 0; j < PPL; ++j) {
+        for (int j = 0; j < PPL; ++j) {
 #if TQSB_RELOAD
-                const int pj = lane + 32 * j;
-                const int pr = pj < B * B ? pj / B : -1, pcc = pj % B;
+            const int pj = lane + 32 * j;
+            const int pr = pj < B * B ? pj / B : -1, pcc = pj % B;
 #else
-                const int pr = p_r[j], pcc = p_c[j];
+            const int pr = p_r[j], pcc = p_c[j];
 #endif
-                if (pr >= 0) {
-                    const int orow = bo.x + pr, ocol = bo.y + pcc;
-                    if (orow < a.out_rows && ocol < a.out_cols) {
-                        float val = acc[j];
-                        if (a.clip) val = fminf(fmaxf(val, 0.f), 1.f);
-                        a.out[size_t(orow - a.out_row0) * a.out_cols + ocol] = double(val);
-                    }
+            if (pr >= 0) {
+                const int orow = bo.x + pr, ocol = bo.y + pcc;
+                if (orow < a.out_rows && ocol < a.out_cols) {
+                    float val = acc[j];
+                    if (a.clip) val = fminf(fmaxf(val, 0.f), 1.f);
+                    a.out[size_t(orow - a.out_row0) * a.out_cols + ocol] = double(val);
                 }
             }
-            if (tracing) {
-                if (lane == 0) *a.trace_n = it;
-                if (a.trace_window) {
-                    __syncwarp();
-                    for (int p = lane; p < W * W; p += 32) {
-                        const int eta = p / W, gam = p % W;
-                        float sacc = 0.f;
-                        for (int q = 0; q < it; ++q) {
-                            const int k = a.trace_picks[q];
-                            const float2 ph = unit[(eta * (k / W) + gam * (k % W)) % W];
-                            sacc = fmaf(float(a.trace_gd[2 * q]), ph.x,
-                                        fmaf(-float(a.trace_gd[2 * q + 1]), ph.y, sacc));
-                        }
-                        a.trace_window[p] = sacc;
+        }
+        if (tracing) {
+            if (lane == 0) *a.trace_n = it;
+            if (a.trace_window) {
+                __syncwarp();
+                for (int p = lane; p < W * W; p += 32) {
+                    const int eta = p / W, gam = p % W;
+                    float sacc = 0.f;
+                    for (int q = 0; q < it; ++q) {
+                        const int k = a.trace_picks[q];
+                        const float2 ph = unit[(eta * (k / W) + gam * (k % W)) % W];
+                        sacc = fmaf(float(a.trace_gd[2 * q]), ph.x,
+                                    fmaf(-float(a.trace_gd[2 * q + 1]), ph.y, sacc));
                     }
+                    a.trace_window[p] = sacc;
                 }
             }
+        }
+    };
+
+    if constexpr (DYN) {
+        // warp-level dynamic scheduling over the class-sorted task list: no CTA-wide
+        // class state (per-rank factors are read through L1), and no tail imbalance
+        // beyond one block per warp
+        for (;;) {
+            int ti = 0;
+            if (lane == 0) ti = atomicAdd(a.counter, 1);
+            ti = __shfl_sync(FULL, ti, 0);
+            if (ti >= a.n_tasks) break;
+            solve_task(ti, a.tabs[__ldg(a.task_cls + ti)]);
+        }
+    } else {
+        for (int it_item = blockIdx.x; it_item < a.n_items; it_item += gridDim.x) {
+            const WorkItem item = a.items[it_item];
+            if (item.cls != s_cls) {  // CTA-uniform: refill the class's on-chip tables
+                tmem_sync_all();
+                const float4* src = reinterpret_cast<const float4*>(a.tabs[item.cls].cpack);
+                if (warp < 4) {  // one warp per TMEM lane quadrant copies the hot columns
+                    for (int j = 0; j < hotn; ++j) {
+    #pragma unroll
+                        for (int i = 0; i < NS; ++i)
+                            tmem_st4(tq + uint32_t(j * 4 * NS + 4 * i), __ldg(src + size_t(j) * COLF4 + i * 32 + lane));
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                }
+                const float* fsrc = a.tabs[item.cls].fac;
+                for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].x = __float_as_int(__ldg(fsrc + r));
+                tmem_sync_all();
+                if (threadIdx.x == 0) s_cls = item.cls;
+                __syncthreads();
+            }
+            const ClassTab ct = a.tabs[item.cls];
+
+            for (int ti = item.start + warp; ti < item.start + item.count; ti += kWarpsF32)
+                solve_task(ti, ct);
         }
     }
     tmem_sync_all();

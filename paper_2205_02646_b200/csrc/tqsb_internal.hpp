@@ -70,6 +70,9 @@ struct SolveArgs {
     const Task* tasks;
     const WorkItem* items;
     int n_items;
+    const int* task_cls;   // class slot per task (warp-level dynamic scheduling)
+    int n_tasks;
+    int* counter;          // next task (zeroed before each launch)
     const ClassTab* tabs;
     WindowConsts wc;
     int window, block, iterations;
