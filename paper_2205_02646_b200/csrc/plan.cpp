@@ -1471,6 +1471,8 @@ int tqsb_plan_block_trace(tqsb_plan* p, int orow, int ocol, const double* y_loca
     a.tasks = d_task;
     a.items = d_item;
     a.n_items = 1;
+    a.n_tasks = 1;
+    a.task_cls = nullptr;  // the single item's class
     a.trace_picks = d_picks;
     a.trace_gd = d_gd;
     a.trace_window = window_out ? d_win : nullptr;

@@ -36,11 +36,11 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a)
     unsigned char* touched = reinterpret_cast<unsigned char*>(order + K);
 
     const int gw = blockIdx.x * kWarpsF64 + warp, nw = gridDim.x * kWarpsF64;
-    for (int it_item = 0; it_item < a.n_items; ++it_item) {
-        const WorkItem item = a.items[it_item];
-        const ClassTab& ct = a.tabs[item.cls];
-        const int L = ct.local;
-        for (int ti = item.start + gw; ti < item.start + item.count; ti += nw) {
+    // every warp strides over the whole class-sorted task list
+    {
+        for (int ti = gw; ti < a.n_tasks; ti += nw) {
+            const ClassTab& ct = a.tabs[a.task_cls ? a.task_cls[ti] : a.items[0].cls];
+            const int L = ct.local;
             const Task tk = a.tasks[ti];
             // gather_local_values (grid.cpp:104-114); pad_frame by clamping (pipeline.cpp:44-52)
             const int r0 = (tk.origin_row + 1) / 2, r1 = (tk.origin_row + W - 2) / 2;

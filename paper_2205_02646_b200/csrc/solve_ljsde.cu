@@ -13,7 +13,11 @@
 // k), on the class's resident B = w T (k-major) and den = D (tables.cu), so its
 // output matches the reference's L-JSDE to ~1e-15 and the RL-JSDE fp64 mode to the
 // reference's own L <-> RL equivalence bar (bench, pipeline.cpp:258-329).
-// One warp per block; synthesis and placement as in solve_f64.cu.
+//
+// One CTA of kThreadsL threads per block: thread j owns frequencies j, j + kThreadsL,
+// ... (each summed over m in order, so the arithmetic per k is the reference's), the
+// first-max selection is a CTA reduction with ties to the smaller k, and the residual
+// (L <= K/4 complex) lives in shared memory. Synthesis and placement as in solve_f64.cu.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,16 +28,27 @@ namespace tqsb {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kWarpsL = 4;
+constexpr int kThreadsL = 256;
+constexpr int kWarpsL = kThreadsL / 32;
 
-__global__ void __launch_bounds__(kWarpsL * 32) k_solve_ljsde(const SolveArgs a) {
+struct Best {
+    double s;
+    int k;
+};
+
+// strict first-max: a candidate wins on a larger score, or an equal score at a smaller k
+__device__ __forceinline__ Best better(Best a, Best b) {
+    if (b.k < 0) return a;
+    if (a.k < 0) return b;
+    return (b.s > a.s || (b.s == a.s && b.k < a.k)) ? b : a;
+}
+
+__global__ void __launch_bounds__(kThreadsL) k_solve_ljsde(const SolveArgs a) {
     extern __shared__ __align__(16) double smL[];
     const int W = a.window, K = W * W, B = a.block;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // per warp: N (2K), coef (2K), r (2 * K/4), order (K ints), touched (K bytes)
-    const size_t per = size_t(4) * K + K / 2 + K / 2 + K / 8 + 8;
-    double* base = smL + warp * per;
-    double* Nr = base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // N (2K), coef (2K), r (2 * (K/4 + 1)), order (K ints), touched (K bytes)
+    double* Nr = smL;
     double* Ni = Nr + K;
     double* cr = Ni + K;
     double* ci = cr + K;
@@ -41,39 +56,40 @@ __global__ void __launch_bounds__(kWarpsL * 32) k_solve_ljsde(const SolveArgs a)
     double* ri = rr + K / 4 + 1;
     int* order = reinterpret_cast<int*>(ri + K / 4 + 1);
     unsigned char* touched = reinterpret_cast<unsigned char*>(order + K);
+    __shared__ Best s_best[kWarpsL];
+    __shared__ int s_stop;
 
-    const int gw = blockIdx.x * kWarpsL + warp, nw = gridDim.x * kWarpsL;
-    for (int it_item = 0; it_item < a.n_items; ++it_item) {
-        const WorkItem item = a.items[it_item];
-        const ClassTab& ct = a.tabs[item.cls];
-        const int L = ct.local;
-        for (int ti = item.start + gw; ti < item.start + item.count; ti += nw) {
+    // every CTA strides over the whole class-sorted task list (a work item holds only a
+    // few dozen tasks, far fewer than the grid's CTAs)
+    {
+        for (int ti = blockIdx.x; ti < a.n_tasks; ti += gridDim.x) {
+            const ClassTab& ct = a.tabs[a.task_cls ? a.task_cls[ti] : a.items[0].cls];
+            const int L = ct.local;
             const Task tk = a.tasks[ti];
             // r = y^local (extract_local_system / gather_local_values, grid.cpp:104-114)
             const int r0 = (tk.origin_row + 1) / 2;
             const int c0 = (tk.origin_col + 1) / 2, c1 = (tk.origin_col + W - 2) / 2;
             const int ncol = c1 - c0 + 1;
-            for (int m = lane; m < L; m += 32) {
+            for (int m = tid; m < L; m += kThreadsL) {
                 int fr = r0 + m / ncol, fc = c0 + m % ncol;
                 fr = fr < a.frame_rows - 1 ? fr : a.frame_rows - 1;
                 fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
                 rr[m] = a.frame[size_t(fr - a.frame_row0) * a.frame_pitch + fc];
                 ri[m] = 0.0;
             }
-            for (int k = lane; k < K; k += 32) {
+            for (int k = tid; k < K; k += kThreadsL) {
                 cr[k] = 0.0;
                 ci[k] = 0.0;
                 touched[k] = 0;
             }
-            __syncwarp();
+            __syncthreads();
             const double floor = a.early_stop ? a.early_stop_scale * L : -1.0;
             const bool tracing = a.trace_picks != nullptr && ti == 0;
             int nactive = 0, it = 0;
             for (; it < a.iterations; ++it) {
                 // numerators for every frequency + first-max selection (score_all)
-                int best = -1;
-                double bs = 0.0;
-                for (int k = lane; k < K; k += 32) {
+                Best best{0.0, -1};
+                for (int k = tid; k < K; k += kThreadsL) {
                     const double* col = ct.b64 + size_t(k) * L * 2;
                     double nr = 0.0, ni = 0.0;
                     for (int m = 0; m < L; ++m) {
@@ -86,29 +102,27 @@ __global__ void __launch_bounds__(kWarpsL * 32) k_solve_ljsde(const SolveArgs a)
                     const double den = ct.d64[k];
                     if (den <= 0.0) continue;
                     const double s = a.wc.q64[k] * (nr * nr + ni * ni) / den;
-                    if (best < 0 || s > bs) {
-                        best = k;
-                        bs = s;
-                    }
+                    if (best.k < 0 || s > best.s) best = Best{s, k};  // k ascending per thread
                 }
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) {
-                    const double os = __shfl_xor_sync(FULL, bs, off);
-                    const int ok = __shfl_xor_sync(FULL, best, off);
-                    const bool take = ok >= 0 && (best < 0 || os > bs || (os == bs && ok < best));
-                    if (take) {
-                        bs = os;
-                        best = ok;
-                    }
+                    Best o;
+                    o.s = __shfl_xor_sync(FULL, best.s, off);
+                    o.k = __shfl_xor_sync(FULL, best.k, off);
+                    best = better(best, o);
                 }
-                if (best < 0) break;  // no admissible frequency
-                __syncwarp();
-                const int u = best;
+                if (lane == 0) s_best[warp] = best;
+                __syncthreads();
+                best = s_best[0];
+#pragma unroll
+                for (int w = 1; w < kWarpsL; ++w) best = better(best, s_best[w]);
+                if (best.k < 0) break;  // no admissible frequency (uniform across the CTA)
+                const int u = best.k;
                 const double den = ct.d64[u];
                 const double gr = a.step * (Nr[u] / den), gi = a.step * (Ni[u] / den);
                 const bool fresh = touched[u] == 0;
-                __syncwarp();
-                if (lane == 0) {
+                __syncthreads();  // all reads of s_best / touched precede the writes below
+                if (tid == 0) {
                     cr[u] += gr;
                     ci[u] += gi;
                     if (fresh) {
@@ -124,29 +138,31 @@ __global__ void __launch_bounds__(kWarpsL * 32) k_solve_ljsde(const SolveArgs a)
                 if (fresh) ++nactive;
                 // r_m -= g conj(T_mu), T from the stored w T (ljsde.cpp:163-170)
                 const double* col = ct.b64 + size_t(u) * L * 2;
-                for (int m = lane; m < L; m += 32) {
+                for (int m = tid; m < L; m += kThreadsL) {
                     const double wm = ct.w64[m];
                     const double tr = col[2 * m] / wm, tim = -col[2 * m + 1] / wm;
                     rr[m] -= gr * tr - gi * tim;
                     ri[m] -= gr * tim + gi * tr;
                 }
-                __syncwarp();
+                __syncthreads();
                 if (a.early_stop) {  // energy stop, summed in m order like the reference
-                    double es = 0.0;
-                    if (lane == 0)
+                    if (tid == 0) {
+                        double es = 0.0;
                         for (int m = 0; m < L; ++m) es += (rr[m] * rr[m] + ri[m] * ri[m]) * ct.w64[m];
-                    es = __shfl_sync(FULL, es, 0);
-                    if (es < floor) {
+                        s_stop = es < floor;
+                    }
+                    __syncthreads();
+                    if (s_stop) {
                         ++it;  // this iteration completed (the hook ran) before the stop
                         break;
                     }
                 }
             }
-            if (tracing && lane == 0) *a.trace_n = it;
-            __syncwarp();
+            if (tracing && tid == 0) *a.trace_n = it;
+            __syncthreads();
             // synthesize_real (basis.cpp:52-73) over the kept pixels, then place
             const int rw = tk.block_row - tk.origin_row, cw = tk.block_col - tk.origin_col;
-            for (int p = lane; p < B * B; p += 32) {
+            for (int p = tid; p < B * B; p += kThreadsL) {
                 const int eta = rw + p / B, gam = cw + p % B;
                 double v = 0.0;
                 for (int t = 0; t < nactive; ++t) {
@@ -161,7 +177,7 @@ __global__ void __launch_bounds__(kWarpsL * 32) k_solve_ljsde(const SolveArgs a)
                 }
             }
             if (tracing && a.trace_window) {
-                for (int p = lane; p < K; p += 32) {
+                for (int p = tid; p < K; p += kThreadsL) {
                     const int eta = p / W, gam = p % W;
                     double v = 0.0;
                     for (int t = 0; t < nactive; ++t) {
@@ -172,7 +188,7 @@ __global__ void __launch_bounds__(kWarpsL * 32) k_solve_ljsde(const SolveArgs a)
                     a.trace_window[p] = v;
                 }
             }
-            __syncwarp();
+            __syncthreads();
         }
     }
 }
@@ -181,12 +197,15 @@ __global__ void __launch_bounds__(kWarpsL * 32) k_solve_ljsde(const SolveArgs a)
 
 int launch_solve_ljsde(const SolveArgs& a, void* stream, int num_sms) {
     const int K = a.window * a.window;
-    const size_t per = size_t(4) * K + K / 2 + K / 2 + K / 8 + 8;
-    const size_t smem = per * sizeof(double) * kWarpsL;
+    const size_t smem = (size_t(4) * K + 2 * (K / 4 + 1) + K / 2 + K / 8 + 8) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_solve_ljsde, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
-    k_solve_ljsde<<<num_sms * 2, kWarpsL * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_ljsde, kThreadsL, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    k_solve_ljsde<<<grid, kThreadsL, smem, static_cast<cudaStream_t>(stream)>>>(a);
     return cudaGetLastError();
 }
 
