@@ -1,5 +1,6 @@
 // solve_common.cuh -- device helpers shared by the fp32 solve kernels
-// (solve_f32.cu: one warp per block; solve_pair.cu: a warp pair per block).
+// (solve_f32.cu): selection keys, the register pick, score and update passes,
+// chunked column loads (global or TMEM) and the TMEM helpers.
 #pragma once
 #include <cuda_runtime.h>
 

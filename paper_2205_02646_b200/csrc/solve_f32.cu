@@ -9,20 +9,25 @@
 //              (B_mk = w_m (1/3) sum_px conj(unit[(eta sigma + gamma rho) mod W])).
 //              Only sigma <= W/2 is computed; the other half is written as the
 //              exact conjugate, so conjugate pairs tie bitwise like the reference's.
-//  loop (K3)   nu x { argmax_k q_k |R_k|^2 / D_k over D_k > 0, smallest k on ties
-//              (rljsde.cpp:144-158, basis.hpp:90-92); R -= gamma (R_u/D_u) C[:,u]
-//              (160-172) } on the SCALED residual R'_k = sqrt(q_k/D_k) R_k, so the
-//              score is |R'_k|^2 and the update streams C'[s,u] = s_s C[s,u] --
-//              2 FFMA2 per complex element, 2 more for the score, FMNMX3 for the max.
+//  loop (K3)   nu x { argmax_k q_k |R_k|^2 / D_k over D_k > 0 (rljsde.cpp:144-158,
+//              basis.hpp:90-92); R -= gamma (R_u/D_u) C[:,u] (160-172) } on the SCALED
+//              residual R'_k = sqrt(q_k/D_k) R_k, so the score is |R'_k|^2 and the update
+//              streams C'[s,u] = s_s C[s,u] -- 2 FFMA2 per complex element, 2 more for the
+//              score. Selection: each score carries its in-lane position in its low 5
+//              mantissa bits (score_key), one FMNMX3 tree + CREDUX give max and position,
+//              a ballot the lane; conjugate pairs sit on one lane's slot halves so their
+//              bitwise ties resolve to the smaller flat k like the reference's.
 //  synth (K4)  only the B x B target pixels of sum Re(g unit[(eta sigma + gamma rho)])
 //              (basis.cpp:52-73 restricted to the kept block, pipeline.cpp:157-166),
 //              accumulated per pick, clipped and stored straight into the output.
 //
 // Register layout: lane j, slot i holds ranks r = 64 i + 2 j + {0,1} as one float4
-// (re_a, re_b, im_a, im_b); ranks order frequencies by centred radius (hot first).
-// The C' column of rank u is the same float4 array, so a column read is 32 lanes x
-// 16 B = one fully coalesced 512 B line per slot. The first `hot` columns of the
-// CTA's class are cached in shared memory; the rest stream from L2.
+// (re_a, re_b, im_a, im_b); ranks order frequencies by centred radius (hot first). The
+// C' column of rank u is the same float4 array, so a column read is 32 lanes x 16 B =
+// one fully coalesced 512 B line per slot, streamed in 4-slot chunks two chunks ahead
+// of the update (L1/L2; optionally the lowest ranks from TMEM, template TM).
+// Scheduling: warps take blocks from a global counter (DYN) -- or, with the TMEM tier
+// or tracing, CTAs stride over 48-block single-class work items.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,12 +38,6 @@
 #ifndef TQSB_KEYS
 #define TQSB_KEYS 1  // packed score/position keys (see score_key)
 #endif
-#ifndef TQSB_UNI
-#define TQSB_UNI 1
-#endif
-#ifndef TQSB_RELOAD
-#define TQSB_RELOAD 0  // re-read the task after the loop instead of holding it in registers
-#endif
 #ifndef TQSB_DYN
 #define TQSB_DYN 1  // warp-level dynamic task scheduling when no CTA-wide class state is needed
 #endif
@@ -46,7 +45,7 @@
 #define TQSB_TIMING 0  // per-phase clock() accounting of the iteration (experiment builds)
 #endif
 #ifndef TQSB_AHEAD
-#define TQSB_AHEAD 2  // 4-slot chunks in flight ahead of the update (TQSB_UNI)
+#define TQSB_AHEAD 2  // 4-slot column chunks in flight ahead of the update (NS == 16)
 #endif
 
 namespace tqsb {
@@ -261,7 +260,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             const int slot = t >> 1, b = t & 1;
             const int u = 64 * slot + 2 * Lw + b;
             // ---- issue the whole C' column now; its latency overlaps the pick ----
-            constexpr bool kUni = NS == 16 && TQSB_UNI;  // one update path for both tiers
+            constexpr bool kUni = NS == 16;  // one chunked update path for both column tiers
             constexpr int PF = kUni ? 4 * TQSB_AHEAD : (NS < TQSB_PREFETCH ? NS : TQSB_PREFETCH);
             float4 c[NS];
             const float4* col = gcols + size_t(u) * COLF4;
@@ -348,20 +347,10 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             for (int q = 0; q < 6; ++q) atomicAdd(&g_tdbg[q], tacc[q]);
 #endif
         // ---- placement: clip + crop straight into the output ----
-#if TQSB_RELOAD
-        // (the task and pixel map are re-read here rather than held across the loop)
-        const int2 bo = *reinterpret_cast<const int2*>(a.tasks + ti);
-#else
         const int2 bo = make_int2(tk.block_row, tk.block_col);
-#endif
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
-#if TQSB_RELOAD
-            const int pj = lane + 32 * j;
-            const int pr = pj < B * B ? pj / B : -1, pcc = pj % B;
-#else
             const int pr = p_r[j], pcc = p_c[j];
-#endif
             if (pr >= 0) {
                 const int orow = bo.x + pr, ocol = bo.y + pcc;
                 if (orow < a.out_rows && ocol < a.out_cols) {
