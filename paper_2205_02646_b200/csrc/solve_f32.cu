@@ -76,8 +76,11 @@ struct Scratch {
     static constexpr int kFloats = (kZ > kR ? (kZ > kS ? kZ : kS) : (kR > kS ? kR : kS));
 };
 
-template <int NS, int W, int PPL, bool TRACE, bool TM>
-__global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs a) {
+// NW warps per CTA (1 CTA per SM): 16 at 128 registers where the kernel fits without
+// spilling (the default W = 32 / B = 4 product path: 38.8 vs 40.5 ms per 4K frame at 12),
+// 12 at 168 registers for the heavier instantiations (B >= 8, TMEM tier, tracing)
+template <int NS, int W, int PPL, bool TRACE, bool TM, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
     constexpr bool DYN = !TRACE && !TM && TQSB_DYN;  // per-warp task queue (a.counter)
     extern __shared__ __align__(16) float smem[];
     constexpr int COLF4 = NS * 32;  // float4 per column
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
             }
             const ClassTab ct = a.tabs[item.cls];
 
-            for (int ti = item.start + warp; ti < item.start + item.count; ti += kWarpsF32)
+            for (int ti = item.start + warp; ti < item.start + item.count; ti += NW)
                 solve_task(ti, ct);
         }
     }
@@ -423,18 +426,20 @@ __global__ void __launch_bounds__(kWarpsF32 * 32, 1) k_solve_f32(const SolveArgs
 
 template <int NS, int W, int PPL>
 int launch_one(const SolveArgs& a, cudaStream_t stream, int num_sms) {
-    const size_t smem = solve_f32_smem_bytes(NS, a.hot) ;
     // the TMEM column tier only when columns are assigned to it (results are identical
     // either way; it costs instructions: measured 40.6 vs 40.1 ms per 4K frame with it on)
-    auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true, false>
-                : a.hot > 0   ? k_solve_f32<NS, W, PPL, false, true>
-                              : k_solve_f32<NS, W, PPL, false, false>;
+    constexpr int NWP = PPL <= 2 ? kWarpsF32 : kWarpsF32Heavy;  // product path
+    const int nw = (a.trace_picks || a.hot > 0) ? kWarpsF32Heavy : NWP;
+    const size_t smem = solve_f32_smem_bytes(NS, nw);
+    auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true, false, kWarpsF32Heavy>
+                : a.hot > 0   ? k_solve_f32<NS, W, PPL, false, true, kWarpsF32Heavy>
+                              : k_solve_f32<NS, W, PPL, false, false, NWP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
     int grid = a.n_items < num_sms ? a.n_items : num_sms;
     if (grid < 1) grid = 1;
-    kern<<<grid, kWarpsF32 * 32, smem, stream>>>(a);
+    kern<<<grid, nw * 32, smem, stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -462,10 +467,9 @@ extern "C" int tqsb_debug_timing(unsigned long long* out) {
 }
 #endif
 
-size_t solve_f32_smem_bytes(int n_slots, int hot) {
+size_t solve_f32_smem_bytes(int n_slots, int warps) {
     // (fac, perm) per rank + unit table + per-warp scratch; hot columns live in TMEM
-    (void)hot;
-    return size_t(n_slots) * 64 * 8 + 32 * 8 + size_t(kWarpsF32) * Scratch<32>::kFloats * 4;
+    return size_t(n_slots) * 64 * 8 + 32 * 8 + size_t(warps) * Scratch<32>::kFloats * 4;
 }
 
 int solve_f32_max_hot(int n_slots, int device) {

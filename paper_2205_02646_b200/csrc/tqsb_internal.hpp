@@ -10,9 +10,10 @@ namespace tqsb {
 
 constexpr int kMaxWindow = 32;  // device paths hold a warp-row per window row/col
 #ifndef TQSB_WARPS_F32
-#define TQSB_WARPS_F32 12
+#define TQSB_WARPS_F32 16
 #endif
 constexpr int kWarpsF32 = TQSB_WARPS_F32;  // warps per CTA of the fp32 solve kernel (1 CTA/SM)
+constexpr int kWarpsF32Heavy = 12;  // ... for its register-heavy instantiations (solve_f32.cu)
 constexpr int kWarpsF64 = 4;    // warps per CTA of the fp64 parity kernel
 constexpr int kSbufStride = 36; // floats per lane in the element-score buffer (conflict-free STS.128)
 
@@ -93,7 +94,7 @@ struct SolveArgs {
 int launch_solve_f32(const SolveArgs& a, int n_slots, void* stream, int num_sms);
 int launch_solve_f64(const SolveArgs& a, void* stream, int num_sms);
 int launch_solve_ljsde(const SolveArgs& a, void* stream, int num_sms);
-size_t solve_f32_smem_bytes(int n_slots, int hot);
+size_t solve_f32_smem_bytes(int n_slots, int warps);
 int solve_f32_max_hot(int n_slots, int device);
 
 // Per-class build descriptor for the batched table kernels (tables.cu).
