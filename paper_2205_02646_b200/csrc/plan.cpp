@@ -85,13 +85,17 @@ int validate(const tqsb_config& c, int period) {
     return TQSB_OK;
 }
 
-// device-path limits (not in the reference): one warp spans a window row/col
+// device-path limits (not in the reference): the fp32 product kernel holds a window
+// row/column per warp (W <= 32); larger windows run on the generic fp64 kernel
 int validate_device_limits(const tqsb_config& c) {
-    if (c.window > kMaxWindow)
-        return set_error(TQSB_EINVAL, "window sizes above 32 are not supported by the device solver");
-    if (c.compute == TQSB_COMPUTE_FP32 && c.block * c.block > 256)
+    if (c.compute == TQSB_COMPUTE_FP32 && c.window <= kMaxWindowF32 && c.block * c.block > 256)
         return set_error(TQSB_EINVAL, "block sizes above 16 require compute=fp64");
     return TQSB_OK;
+}
+
+// the fp32 product kernel serves the plan (else the fp64 kernel: compute=fp64, or W > 32)
+bool uses_f32(const tqsb_config& c) {
+    return c.compute == TQSB_COMPUTE_FP32 && c.window <= kMaxWindowF32;
 }
 
 struct Geometry {
@@ -154,7 +158,7 @@ void enumerate(const Geometry& g, int period, int br_begin, int br_end, Enumerat
 // ---------------------------------------------------------------------------
 struct LocalSystem {
     int L = 0;
-    std::vector<signed char> px;   // L*6
+    std::vector<short> px;         // L*6
     std::vector<double> w;         // L
     std::vector<float> mask32;     // W*W
 };
@@ -177,8 +181,8 @@ LocalSystem local_system(const std::vector<uint8_t>& opaque, int period, int oro
             for (int quad = 0; quad < 4; ++quad) {  // transparent quadrants, row-major
                 if (quad == q) continue;
                 const int eta = ce + quad / 2, gam = cg + quad % 2;
-                s.px.push_back(static_cast<signed char>(eta));
-                s.px.push_back(static_cast<signed char>(gam));
+                s.px.push_back(static_cast<short>(eta));
+                s.px.push_back(static_cast<short>(gam));
                 s.mask32[size_t(eta) * W + gam] = float(w * (1.0 / 3.0));
             }
             ++s.L;
@@ -203,7 +207,9 @@ WindowTables window_tables(const tqsb_config& c) {
     t.W = W;
     t.K = W * W;
     const int ns = (t.K + 63) / 64;
-    t.NS = ns <= 1 ? 1 : ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 8 ? 8 : 16;
+    // fp32 register slots per lane (power of two, W <= 32); above that the rank tables
+    // only need to cover K (the fp64 kernel does not use them)
+    t.NS = ns <= 1 ? 1 : ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 8 ? 8 : ns <= 16 ? 16 : ns;
     t.K_pad = 64 * t.NS;
     t.unit64.assign(2 * W, 0.0);
     t.unit64[0] = 1.0;
@@ -433,6 +439,7 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
 int alloc_class(tqsb_plan* p, Device* d, int key, int orow, int ocol, ClassBuild* cb) {
     const WindowTables& t = p->wt;
     const size_t K = t.K, K_pad = t.K_pad, W = t.W;
+    const bool f32 = uses_f32(p->cfg);  // fp32 product tables only for the fp32 kernel
     LocalSystem ls = local_system(p->opaque, p->period, orow, ocol, p->cfg);
     const size_t L = ls.L;
     size_t off = 0;
@@ -443,29 +450,29 @@ int alloc_class(tqsb_plan* p, Device* d, int key, int orow, int ocol, ClassBuild
     };
     const size_t o_c64 = take(K * K * 2 * 8), o_b64 = take(K * L * 2 * 8),
                  o_t64 = take(K * L * 2 * 8), o_d64 = take(K * 8),
-                 o_cpack = take(K_pad * K_pad * 8), o_scale = take(K_pad * 4),
-                 o_fac = take(K_pad * 4), o_mask = take(W * W * 4), o_px = take(L * 6 + 8),
+                 o_cpack = f32 ? take(K_pad * K_pad * 8) : 0, o_scale = f32 ? take(K_pad * 4) : 0,
+                 o_fac = f32 ? take(K_pad * 4) : 0, o_mask = take(W * W * 4), o_px = take(L * 12 + 8),
                  o_w = take(L * 8 + 8);
     ClassSlab slab;
     slab.bytes = off;
     CUDA_TRY(cudaMalloc(&slab.base, slab.bytes));
     char* b = static_cast<char*>(slab.base);
-    CUDA_TRY(cudaMemcpyAsync(b + o_px, ls.px.data(), L * 6, cudaMemcpyHostToDevice, d->stream));
+    CUDA_TRY(cudaMemcpyAsync(b + o_px, ls.px.data(), L * 12, cudaMemcpyHostToDevice, d->stream));
     CUDA_TRY(cudaMemcpyAsync(b + o_w, ls.w.data(), L * 8, cudaMemcpyHostToDevice, d->stream));
     CUDA_TRY(cudaMemcpyAsync(b + o_mask, ls.mask32.data(), W * W * 4, cudaMemcpyHostToDevice,
                              d->stream));
     CUDA_TRY(cudaStreamSynchronize(d->stream));  // host vectors die at scope end
     *cb = ClassBuild{};
     cb->local = int(L);
-    cb->px = reinterpret_cast<const signed char*>(b + o_px);
+    cb->px = reinterpret_cast<const short*>(b + o_px);
     cb->w = reinterpret_cast<const double*>(b + o_w);
     cb->t64 = reinterpret_cast<double*>(b + o_t64);
     cb->b64 = reinterpret_cast<double*>(b + o_b64);
     cb->c64 = reinterpret_cast<double*>(b + o_c64);
     cb->d64 = reinterpret_cast<double*>(b + o_d64);
-    cb->cpack = reinterpret_cast<float*>(b + o_cpack);
-    cb->scale = reinterpret_cast<float*>(b + o_scale);
-    cb->fac = reinterpret_cast<float*>(b + o_fac);
+    cb->cpack = f32 ? reinterpret_cast<float*>(b + o_cpack) : nullptr;
+    cb->scale = f32 ? reinterpret_cast<float*>(b + o_scale) : nullptr;
+    cb->fac = f32 ? reinterpret_cast<float*>(b + o_fac) : nullptr;
     ClassTab tab{};
     tab.cpack = cb->cpack;
     tab.scale = cb->scale;
@@ -644,7 +651,7 @@ SolveArgs base_args(tqsb_plan* p, Device* d) {
 int launch(tqsb_plan* p, Device* d, const SolveArgs& a, cudaStream_t s) {
     if (a.counter) CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
     int rc = p->cfg.algorithm == TQSB_ALGO_LJSDE ? launch_solve_ljsde(a, s, d->num_sms)
-             : p->cfg.compute == TQSB_COMPUTE_FP32 ? launch_solve_f32(a, p->wt.NS, s, d->num_sms)
+             : uses_f32(p->cfg)                    ? launch_solve_f32(a, p->wt.NS, s, d->num_sms)
                                                    : launch_solve_f64(a, s, d->num_sms);
     if (rc != 0)
         return set_error(TQSB_ECUDA, std::string("solve launch: ") +

@@ -13,6 +13,8 @@
 
 #include <cstdint>
 
+#include <cstdlib>
+
 #include "tqsb_internal.hpp"
 
 namespace tqsb {
@@ -20,13 +22,18 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a) {
+// per-warp state in doubles: R (2K), coef (2K), y (K), order (K ints), touched (K bytes)
+__host__ __device__ inline size_t f64_state_doubles(int K) { return size_t(5) * K + K / 2 + K / 8 + 8; }
+
+// State in shared memory (warps per CTA chosen by the launcher to fit), or, for windows
+// whose state exceeds shared memory (W >= 68), in a global scratch slab (gscratch).
+__global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a, double* gscratch) {
     extern __shared__ __align__(16) double sm64[];
     const int W = a.window, K = W * W, B = a.block;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // per warp: R (2K), coef (2K), y (K/4+..: use K), order (K ints), touched (K bytes)
-    const size_t per = size_t(5) * K + K / 2 + K / 8 + 8;
-    double* base = sm64 + warp * per;
+    const int wpc = blockDim.x >> 5;  // warps per CTA
+    const size_t per = f64_state_doubles(K);
+    double* base = gscratch ? gscratch + (size_t(blockIdx.x) * wpc + warp) * per : sm64 + warp * per;
     double* Rr = base;
     double* Ri = Rr + K;
     double* cr = Ri + K;
@@ -35,7 +42,7 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a)
     int* order = reinterpret_cast<int*>(y + K);
     unsigned char* touched = reinterpret_cast<unsigned char*>(order + K);
 
-    const int gw = blockIdx.x * kWarpsF64 + warp, nw = gridDim.x * kWarpsF64;
+    const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
     // every warp strides over the whole class-sorted task list
     {
         for (int ti = gw; ti < a.n_tasks; ti += nw) {
@@ -163,15 +170,31 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a)
 } // namespace
 
 int launch_solve_f64(const SolveArgs& a, void* stream, int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int K = a.window * a.window;
-    const size_t per = size_t(5) * K + K / 2 + K / 8 + 8;
-    const size_t smem = per * sizeof(double) * kWarpsF64;
-    cudaError_t e = cudaFuncSetAttribute(k_solve_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
+    const size_t per_bytes = f64_state_doubles(K) * sizeof(double);
+    constexpr size_t kSmemMax = 227 * 1024;
+    // as many warps per CTA (<= kWarpsF64) as shared memory holds; none -> global state
+    int wpc = int(kSmemMax / per_bytes);
+    wpc = wpc > kWarpsF64 ? kWarpsF64 : wpc;
+    if (force_global_state()) wpc = 0;  // test hook: exercise the large-window path
+    const int grid = num_sms * 2;
+    if (wpc >= 1) {
+        const size_t smem = per_bytes * wpc;
+        cudaError_t e = cudaFuncSetAttribute(k_solve_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem));
+        if (e != cudaSuccess) return e;
+        k_solve_f64<<<grid, wpc * 32, smem, st>>>(a, nullptr);
+        return cudaGetLastError();
+    }
+    wpc = kWarpsF64;
+    double* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, per_bytes * size_t(grid) * wpc, st);
     if (e != cudaSuccess) return e;
-    int grid = num_sms * 2;
-    k_solve_f64<<<grid, kWarpsF64 * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
-    return cudaGetLastError();
+    k_solve_f64<<<grid, wpc * 32, 0, st>>>(a, scratch);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaFreeAsync(scratch, st);
 }
 
 } // namespace tqsb

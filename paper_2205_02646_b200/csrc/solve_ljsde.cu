@@ -43,9 +43,16 @@ __device__ __forceinline__ Best better(Best a, Best b) {
     return (b.s > a.s || (b.s == a.s && b.k < a.k)) ? b : a;
 }
 
-__global__ void __launch_bounds__(kThreadsL) k_solve_ljsde(const SolveArgs a) {
-    extern __shared__ __align__(16) double smL[];
+// per-CTA state in doubles (see the layout below)
+__host__ __device__ inline size_t ljsde_state_doubles(int K) {
+    return size_t(4) * K + 2 * (K / 4 + 1) + K / 2 + K / 8 + 8;
+}
+
+// state in shared memory, or in a global slab (gscratch) when it exceeds shared memory
+__global__ void __launch_bounds__(kThreadsL) k_solve_ljsde(const SolveArgs a, double* gscratch) {
+    extern __shared__ __align__(16) double smL_dyn[];
     const int W = a.window, K = W * W, B = a.block;
+    double* smL = gscratch ? gscratch + size_t(blockIdx.x) * ljsde_state_doubles(K) : smL_dyn;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // N (2K), coef (2K), r (2 * (K/4 + 1)), order (K ints), touched (K bytes)
     double* Nr = smL;
@@ -196,8 +203,18 @@ __global__ void __launch_bounds__(kThreadsL) k_solve_ljsde(const SolveArgs a) {
 }  // namespace
 
 int launch_solve_ljsde(const SolveArgs& a, void* stream, int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int K = a.window * a.window;
-    const size_t smem = (size_t(4) * K + 2 * (K / 4 + 1) + K / 2 + K / 8 + 8) * sizeof(double);
+    const size_t smem = ljsde_state_doubles(K) * sizeof(double);
+    if (smem > 227 * 1024 || force_global_state()) {  // W >= 74: state in global memory, one CTA per SM
+        double* scratch = nullptr;
+        cudaError_t e = cudaMallocAsync(&scratch, smem * size_t(num_sms), st);
+        if (e != cudaSuccess) return e;
+        k_solve_ljsde<<<num_sms, kThreadsL, 0, st>>>(a, scratch);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        return cudaFreeAsync(scratch, st);
+    }
     cudaError_t e = cudaFuncSetAttribute(k_solve_ljsde, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
@@ -205,7 +222,7 @@ int launch_solve_ljsde(const SolveArgs& a, void* stream, int num_sms) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_ljsde, kThreadsL, smem);
     if (e != cudaSuccess) return e;
     const int grid = num_sms * (per_sm > 0 ? per_sm : 1);
-    k_solve_ljsde<<<grid, kThreadsL, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    k_solve_ljsde<<<grid, kThreadsL, smem, st>>>(a, nullptr);
     return cudaGetLastError();
 }
 

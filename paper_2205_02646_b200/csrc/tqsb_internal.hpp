@@ -5,10 +5,12 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 
 namespace tqsb {
 
-constexpr int kMaxWindow = 32;  // device paths hold a warp-row per window row/col
+constexpr int kMaxWindowF32 = 32;  // fp32 product kernel: a warp-row per window row/col;
+                                  // larger windows run on the generic fp64 kernel
 #ifndef TQSB_WARPS_F32
 #define TQSB_WARPS_F32 16
 #endif
@@ -90,6 +92,14 @@ struct SolveArgs {
     int* trace_n;
 };
 
+// test hook (env TQSB_FORCE_GLOBAL_STATE=1): the fp64 / L-JSDE kernels keep their
+// per-block state in global memory even when it fits in shared memory, so the
+// large-window path (W >= 68) is exercised at sizes the CPU reference finishes quickly
+inline bool force_global_state() {
+    const char* v = std::getenv("TQSB_FORCE_GLOBAL_STATE");
+    return v && v[0] == '1';
+}
+
 // ---- launchers (defined in the .cu files); return cudaError_t as int ----
 int launch_solve_f32(const SolveArgs& a, int n_slots, void* stream, int num_sms);
 int launch_solve_f64(const SolveArgs& a, void* stream, int num_sms);
@@ -100,7 +110,7 @@ int solve_f32_max_hot(int n_slots, int device);
 // Per-class build descriptor for the batched table kernels (tables.cu).
 struct ClassBuild {
     int local;                 // L
-    const signed char* px;     // L*6: (eta, gamma) of the 3 transparent pixels per cell
+    const short* px;           // L*6: (eta, gamma) of the 3 transparent pixels per cell
     const double* w;           // L spatial weights (host-computed, basis.cpp:75-88)
     double* t64;               // K*L*2 (re, im interleaved), k-major
     double* b64;               // K*L*2
