@@ -77,7 +77,7 @@ struct Scratch {
 };
 
 // NW warps per CTA (1 CTA per SM): 16 at 128 registers where the kernel fits without
-// spilling (the default W = 32 / B = 4 product path: 38.8 vs 40.5 ms per 4K frame at 12),
+// spilling in the loop (the default W = 32 / B = 4 product path: 38.8 vs 40.5 ms per 4K frame at 12),
 // 12 at 168 registers for the heavier instantiations (B >= 8, TMEM tier, tracing)
 template <int NS, int W, int PPL, bool TRACE, bool TM, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
     // KP x (gamma/(s_u D_u) bits, flat k) per rank u
     int2* s_meta = reinterpret_cast<int2*>(smem);
     float2* unit = reinterpret_cast<float2*>(s_meta + KP);   // W (cos, sin)
-    float* scr_all = reinterpret_cast<float*>(unit + 32);
+    float4* unit4 = reinterpret_cast<float4*>(unit + 32);    // W (cos, -sin, sin, -sin): init
+    float* scr_all = reinterpret_cast<float*>(unit4 + 32);
     __shared__ int s_cls;
     __shared__ uint32_t s_tmem;
 
@@ -98,8 +99,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
     float2* zbuf = reinterpret_cast<float2*>(scr);
     float* srow = scr + lane * kSbufStride;  // this lane's element scores
 
-    if (threadIdx.x < W)
-        unit[threadIdx.x] = make_float2(a.wc.unit32[2 * threadIdx.x], a.wc.unit32[2 * threadIdx.x + 1]);
+    if (threadIdx.x < W) {
+        const float cs = a.wc.unit32[2 * threadIdx.x], sn = a.wc.unit32[2 * threadIdx.x + 1];
+        unit[threadIdx.x] = make_float2(cs, sn);
+        unit4[threadIdx.x] = make_float4(cs, -sn, sn, -sn);
+    }
     for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].y = a.wc.perm[r];
     if (threadIdx.x == 0) s_cls = -1;
     // TMEM tier: a.hot columns x 4*NS TMEM columns per quadrant (512 max)
@@ -152,14 +156,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         constexpr int H = W / 2 + 1;
 #pragma unroll
         for (int sg = 0; sg < H; ++sg) {
-            float zr = 0.f, zi = 0.f;
+            // (zr, zi) += (a, -a) * (cos, sin): one FFMA2, the same two roundings as
+            // the scalar pair
+            float2 z = make_float2(0.f, 0.f);
 #pragma unroll
             for (int eta = 0; eta < W; ++eta) {
-                const float2 u = unit[(eta * sg) % W];
-                zr = fmaf(colv[eta], u.x, zr);
-                zi = fmaf(-colv[eta], u.y, zi);
+                const float4 u = unit4[(eta * sg) % W];  // (cos, -sin, sin, -sin)
+                z = __ffma2_rn(make_float2(colv[eta], colv[eta]), make_float2(u.x, u.y), z);
             }
-            zbuf[lane * 18 + sg] = make_float2(zr, zi);
+            zbuf[lane * 18 + sg] = z;
         }
         __syncwarp();
         // step 2 (lane = rho): R0(sigma, rho) = sum_gamma Z(sigma,gamma) conj(U(gamma rho))
@@ -168,12 +173,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         for (int sg = 0; sg < H; ++sg) r0[sg] = make_float2(0.f, 0.f);
 #pragma unroll 4
         for (int g = 0; g < W; ++g) {
-            const float2 u = unit[(g * lane) % W];
+            const float4 u = unit4[(g * lane) % W];
 #pragma unroll
             for (int sg = 0; sg < H; ++sg) {
+                // r0 += (z.y, -z.x) * sin, then += (z.x, z.y) * cos: the scalar FMA order
+                // (inner product with sin first) as two FFMA2
                 const float2 z = zbuf[g * 18 + sg];
-                r0[sg].x = fmaf(z.x, u.x, fmaf(z.y, u.y, r0[sg].x));
-                r0[sg].y = fmaf(z.y, u.x, fmaf(-z.x, u.y, r0[sg].y));
+                const float2 t = __ffma2_rn(make_float2(z.y, z.x), make_float2(u.z, u.w), r0[sg]);
+                r0[sg] = __ffma2_rn(z, make_float2(u.x, u.x), t);
             }
         }
         __syncwarp();
@@ -428,7 +435,7 @@ template <int NS, int W, int PPL>
 int launch_one(const SolveArgs& a, cudaStream_t stream, int num_sms) {
     // the TMEM column tier only when columns are assigned to it (results are identical
     // either way; it costs instructions: measured 40.6 vs 40.1 ms per 4K frame with it on)
-    constexpr int NWP = PPL <= 2 ? kWarpsF32 : kWarpsF32Heavy;  // product path
+    constexpr int NWP = PPL == 1 ? kWarpsF32 : kWarpsF32Heavy;  // product path (B <= 5)
     const int nw = (a.trace_picks || a.hot > 0) ? kWarpsF32Heavy : NWP;
     const size_t smem = solve_f32_smem_bytes(NS, nw);
     auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true, false, kWarpsF32Heavy>
@@ -469,7 +476,7 @@ extern "C" int tqsb_debug_timing(unsigned long long* out) {
 
 size_t solve_f32_smem_bytes(int n_slots, int warps) {
     // (fac, perm) per rank + unit table + per-warp scratch; hot columns live in TMEM
-    return size_t(n_slots) * 64 * 8 + 32 * 8 + size_t(warps) * Scratch<32>::kFloats * 4;
+    return size_t(n_slots) * 64 * 8 + 32 * 8 + 32 * 16 + size_t(warps) * Scratch<32>::kFloats * 4;
 }
 
 int solve_f32_max_hot(int n_slots, int device) {
