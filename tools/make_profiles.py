@@ -115,6 +115,62 @@ def full(tag, out, witers):
               open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 
 
+def raw_lines(tag, out):
+    """The bench lines of tools/evidence.sh (headline, reference arm, period sweep, video,
+    L-JSDE comparison) copied under profiles/ and the sweep/video summary refreshed."""
+    import re
+    import shutil
+
+    def cp(src, dst, last_line=False):
+        path = os.path.join(G, src)
+        if not os.path.exists(path):
+            return None
+        text = open(path).read().strip().splitlines()[-1] if last_line else None
+        if last_line:
+            open(os.path.join(P, dst), "w").write(text + "\n")
+        else:
+            shutil.copy(path, os.path.join(P, dst))
+        return json.loads(open(os.path.join(P, dst)).read().strip().splitlines()[-1])
+
+    cp(f"{tag}_bench.json", f"{out}_bench_4k.json", True)
+    cp(f"{tag}_bench_reference.json", f"{out}_bench_reference_4k.json", True)
+    sweep = {p: cp(f"{tag}_sweep_p{p}.json", f"{out}_bench_1mp_p{p}.json", True) for p in (4, 8, 16, 32)}
+    v = cp(f"{tag}_video.json", f"{out}_bench_video.json", True)
+    lj = cp(f"{tag}_ljsde.json", f"{out}_ljsde_vs_rljsde.json", True)
+    doc_path = os.path.join(P, f"{out}_period_sweep_video.md")
+    if not os.path.exists(doc_path) or any(x is None for x in sweep.values()) or v is None or lj is None:
+        return
+    doc = open(doc_path).read()
+    doc = re.sub(r"Files: `gpurun_out/\w+_\*` of `bash tools/evidence.sh \w+`[^)]*\)",
+                 f"Files: `gpurun_out/{tag}_*` of `bash tools/evidence.sh {tag}` (copied here as this summary)", doc)
+    names = {4: "2x2 (P=4)", 8: "4x4 (P=8)", 16: "8x8 (P=16)", 32: "16x16 (P=32)"}
+    for p, d in sweep.items():
+        c = d["cpu_baseline"]
+        row = (f"| {names[p]} | {d['value']:.1f} | {d['e2e']['value']:.1f} | {d['warm_seconds']:.2f} | "
+               f"{c['value']:.3f} ({c['cores']} cores) | {d['e2e']['value'] / c['value']:.0f}x | "
+               f"{d['roofline']['frac']:.3f} / {d['roofline']['frac_nominal']:.3f} |")
+        doc = re.sub(r"^\| " + re.escape(names[p]) + r" \|.*$", row, doc, flags=re.M)
+    doc = re.sub(r"\| device-resident frames \(`value`\) \| [0-9.]+ \| [0-9.]+ \|",
+                 f"| device-resident frames (`value`) | {v['value']:.1f} | {v['ms_per_step']:.1f} |", doc)
+    doc = re.sub(r"(\| host frames through `tqsb_reconstruct_batch`[^|]*\|) [0-9.]+ \| [0-9.]+ \|",
+                 lambda m: f"{m.group(1)} {v['e2e']['value']:.1f} | {v['e2e']['ms_per_step']:.1f} |", doc)
+    doc = re.sub(r"(\| sensor in the loop[^|]*\|) [0-9.]+ \| [0-9.]+ \|",
+                 lambda m: f"{m.group(1)} {v['device_stream']['value']:.1f} | {v['device_stream']['ms_per_step']:.1f} |", doc)
+    doc = re.sub(r"Roofline frac [0-9.]+ of the measured FFMA2 peak.",
+                 f"Roofline frac {v['roofline']['frac']:.3f} of the measured FFMA2 peak.", doc)
+    doc = re.sub(r"\| reference L-JSDE \| [0-9.]+ \|", f"| reference L-JSDE | {lj['reference_ljsde_s']:.3f} |", doc)
+    doc = re.sub(r"\| reference RL-JSDE \(block phase\) \| [0-9.]+ \|",
+                 f"| reference RL-JSDE (block phase) | {lj['reference_rljsde_s']:.4f} |", doc)
+    doc = re.sub(r"\| device L-JSDE \(fp64, reference summation order\) \| [0-9.]+ \| [0-9.]+x faster; max-abs [0-9.e-]+",
+                 f"| device L-JSDE (fp64, reference summation order) | {lj['gpu_ljsde_s']:.3f} | "
+                 f"{lj['gpu_ljsde_speedup_vs_reference_ljsde']:.1f}x faster; max-abs {lj['gpu_ljsde_max_abs_vs_reference']:.1e}", doc)
+    doc = re.sub(r"\| device RL-JSDE fp64 parity mode \| [0-9.]+ \| L <-> RL max-abs [0-9.e-]+",
+                 f"| device RL-JSDE fp64 parity mode | {lj['gpu_rljsde_fp64_s']:.4f} | L <-> RL max-abs {lj['gpu_l_vs_rl_fp64_max_abs']:.1e}", doc)
+    doc = re.sub(r"\| device RL-JSDE fp32 product path \| [0-9.]+ \| [0-9]+x faster",
+                 f"| device RL-JSDE fp32 product path | {lj['gpu_rljsde_fp32_s']:.5f} | {lj['gpu_rl_fp32_speedup_vs_gpu_ljsde']:.0f}x faster", doc)
+    open(doc_path, "w").write(doc)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("tag")
@@ -124,6 +180,7 @@ def main():
     a = ap.parse_args()
     launches(a.tag, a.out)
     full(a.tag, a.out, a.blocks * a.iters)
+    raw_lines(a.tag, a.out)
 
 
 if __name__ == "__main__":
