@@ -54,7 +54,9 @@ extern "C" {
  * SolverOptions (basis.hpp:77-82) and WeightingConfig (basis.hpp:15-18) inlined.
  * `threads` has no device meaning; the device set is given to tqsb_plan_create. */
 typedef struct tqsb_config {
-    int window;                /* W, default 32 (pipeline.hpp:18) */
+    int window;                /* W, default 32 (pipeline.hpp:18); any even W >= 2 like the
+                                  reference -- W > 32 runs on the fp64 kernel in either
+                                  compute mode */
     int block;                 /* B, default 4 (pipeline.hpp:19) */
     int max_iterations;        /* nu, default 200 (basis.hpp:78) */
     double step_width;         /* gamma_odc in (0,1], default 0.5 (basis.hpp:79) */
@@ -63,7 +65,7 @@ typedef struct tqsb_config {
     int precision;             /* TQSB_PRECISION_*, default DOUBLE (pipeline.hpp:22) */
     int clip_output;           /* default 1 (pipeline.hpp:23) */
     int threads;               /* accepted and validated (>= 0) like the reference; unused */
-    int compute;               /* TQSB_COMPUTE_*, default FP32 */
+    int compute;               /* TQSB_COMPUTE_*, default FP32 (the product kernel, W <= 32) */
     int hot_columns;           /* C' columns held in tensor memory; -1 = auto */
     int algorithm;             /* TQSB_ALGO_*, default RLJSDE (pipeline.hpp:15, 25) */
     int early_stop;            /* L-JSDE energy stop (basis.hpp:80), default 0 */
