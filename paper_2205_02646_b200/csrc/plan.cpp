@@ -98,6 +98,12 @@ bool uses_f32(const tqsb_config& c) {
     return c.compute == TQSB_COMPUTE_FP32 && c.window <= kMaxWindowF32;
 }
 
+// the fp64 RL-JSDE kernel on Precision::Single planes, like the reference's float
+// KernelPlanes (the fp32 product builds its own tables; L-JSDE uses no planes there)
+int round_single(const tqsb_config& c) {
+    return c.precision == TQSB_PRECISION_SINGLE && c.algorithm == TQSB_ALGO_RLJSDE && !uses_f32(c);
+}
+
 struct Geometry {
     int M, N, padM, padN, lead, B, W;
 };
@@ -527,7 +533,7 @@ int ensure_classes(tqsb_plan* p, Device* d, const std::vector<int>& keys,
     }
     int rc = launch_tables_batch(descs.data(), int(descs.size()), p->wt.W, p->wt.K_pad,
                                  p->cfg.step_width, d->d_unit64, d->d_q64, d->d_perm, max_local,
-                                 d->stream, launches, 0);
+                                 d->stream, launches, 0, round_single(p->cfg));
     if (rc != 0) return set_error(TQSB_ECUDA, std::string("table build: ") +
                                                   cudaGetErrorString(cudaError_t(rc)));
     return publish_tabs(d);
@@ -1404,7 +1410,7 @@ int tqsb_plan_load_tables(tqsb_plan* p, const char* path, int* classes_out) {
             int launches = 0;
             const int rc = launch_tables_batch(&cb, 1, window, p->wt.K_pad, p->cfg.step_width,
                                                d->d_unit64, d->d_q64, d->d_perm, cb.local,
-                                               d->stream, &launches, 1);
+                                               d->stream, &launches, 1, round_single(p->cfg));
             if (rc != 0)
                 return set_error(TQSB_ECUDA, std::string("table derive: ") +
                                                  cudaGetErrorString(cudaError_t(rc)));

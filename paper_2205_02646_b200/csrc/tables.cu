@@ -198,12 +198,28 @@ __global__ void k_pack32(const ClassBuild* __restrict__ cls, int W, int k_pad,
     reinterpret_cast<float4*>(c.cpack)[size_t(ur) * (k_pad / 2) + pair] = v;
 }
 
+// The reference's Precision::Single planes (fill_planes<float>, rljsde.cpp:70-100): B, C
+// and D stored as float from the double accumulations, widened to double in the loop
+// (KernelPlanes::dAt and the update's casts) -- here rounded in place in the fp64 planes.
+__global__ void k_round_single(const ClassBuild* __restrict__ cls, int W) {
+    const ClassBuild c = cls[blockIdx.z];
+    const size_t K = size_t(W) * W;
+    const size_t nb = K * c.local * 2, nc = K * K * 2;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nc; i += stride) {
+        c.c64[i] = double(float(c.c64[i]));
+        if (i < nb) c.b64[i] = double(float(c.b64[i]));
+        if (i < K) c.d64[i] = double(float(c.d64[i]));
+    }
+}
+
 } // namespace
 
 // Batched build over n classes; `descs` is a host array copied to the device here.
 int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, double step,
                         const double* unit64, const double* q64, const int* perm,
-                        int max_local, void* stream_, int* launches, int derived_only) {
+                        int max_local, void* stream_, int* launches, int derived_only,
+                        int round_single) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     const ClassBuild* hd = static_cast<const ClassBuild*>(host_descs);
     ClassBuild* dd = nullptr;
@@ -230,6 +246,11 @@ int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, do
                 k_diag<<<g, 256, 0, stream>>>(d, window);
             }
             if (launches) *launches += 3;
+        }
+        if (round_single) {
+            dim3 g(4 * 148, 1, nz);
+            k_round_single<<<g, 256, 0, stream>>>(d, window);
+            if (launches) *launches += 1;
         }
         {
             dim3 g((k_pad + 255) / 256, 1, nz);

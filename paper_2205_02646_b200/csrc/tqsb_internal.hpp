@@ -122,9 +122,11 @@ struct ClassBuild {
 };
 // derived_only: b64 / c64 / d64 are already on the device (loaded TQSK planes);
 // only the fp32 product tables (k_scale, k_pack32) are derived from them.
+// round_single: store B, C, D rounded to float (the reference's Precision::Single).
 int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, double step,
                         const double* unit64, const double* q64, const int* perm,
-                        int max_local, void* stream, int* launches, int derived_only);
+                        int max_local, void* stream, int* launches, int derived_only,
+                        int round_single);
 
 int probe_peaks(int device, double* fp32_tflops, double* smem_tbps);
 

@@ -307,3 +307,27 @@ def test_batch_matches_single_frames(tq, need_gpu):
         finally:
             for p in ptrs:
                 tq.lib.tqsb_host_free(p)
+
+
+@pytest.mark.parametrize("rows,P,W", [(128, 8, 32), (64, 16, 16)])
+def test_fp64_single_precision_matches_reference_single(tq, ref, need_gpu, rows, P, W):
+    """precision = Single with the fp64 kernel: B, C, D held as float from the double
+    accumulations (fill_planes<float>, rljsde.cpp:70-100), double arithmetic in the loop
+    -- the reference's Precision::Single path, to the fp64 mode's 1e-9 bar."""
+    img = tq.synthetic_image(rows, rows, 300 + rows)
+    pat = tq.generate_pattern(7, P)
+    frame = tq.simulate_measurement(img, pat)
+    want, _ = ref.reconstruct(frame, pat.opaque, P, window=W, iterations=200, clip=False,
+                              double=False, threads=0)
+    dbl, _ = ref.reconstruct(frame, pat.opaque, P, window=W, iterations=200, clip=False,
+                             double=True, threads=0)
+    cfg = tq.ReconstructionConfig(window=W, clip_output=False, compute=tq.COMPUTE_FP64,
+                                  precision=tq.PRECISION_SINGLE)
+    with tq.Plan(pat, cfg) as plan:
+        rep = plan.reconstruct(frame)
+        tabs = plan.export_tables(0, 0)
+    assert np.abs(rep.output - want).max() <= 1e-9
+    assert np.abs(want - dbl).max() > 1e-8  # the two reference modes are distinguishable
+    single = ref.precompute(pat.opaque, P, 0, 0, W, double=False)
+    assert np.array_equal(tabs["c"], single["c"]) and np.array_equal(tabs["d"], single["d"])
+    assert np.array_equal(tabs["b"], single["b"])
