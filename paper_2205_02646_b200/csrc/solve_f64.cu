@@ -6,7 +6,11 @@
 // strict '>' first-max rule (144-158, basis.hpp:90-92), the coefficient step and
 // column cascade (160-172), then synthesize_real (basis.cpp:52-73) restricted to
 // the kept B x B pixels over the active list in first-touch order, placement
-// with optional clip (pipeline.cpp:157-166). Its purpose is to prove that the
+// with optional clip (pipeline.cpp:157-166). Every floating-point expression is spelled
+// with explicit-rounding intrinsics in the reference build's own contraction pattern (g++
+// -O3 with FMA: init R += rnd(B y) unfused; score = q * fma(Re, Re, Im*Im) / d; R -= fma(g_re, c_re, -(g_im*c_im))
+// and fma(g_re, c_im, g_im*c_re); synthesis += fma(c_re, cos, -(c_im*sin))), so the
+// greedy paths match the reference's even at near-ties. Its purpose is to prove that the
 // device pipeline (enumeration, classes, tables, gather, placement) reproduces
 // the reference's greedy paths; the fp32 kernel (solve_f32.cu) is the product.
 #include <cuda_runtime.h>
@@ -48,6 +52,7 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a,
         for (int ti = gw; ti < a.n_tasks; ti += nw) {
             const ClassTab& ct = a.tabs[a.task_cls ? a.task_cls[ti] : a.items[0].cls];
             const int L = ct.local;
+            const int n_unfused = 8 * (L / 8) + (L % 8 >= 4 ? 4 : 0);
             const Task tk = a.tasks[ti];
             // gather_local_values (grid.cpp:104-114); pad_frame by clamping (pipeline.cpp:44-52)
             const int r0 = (tk.origin_row + 1) / 2, r1 = (tk.origin_row + W - 2) / 2;
@@ -70,8 +75,17 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a,
                 const double* col = ct.b64 + size_t(k) * L * 2;
                 double re = 0.0, im = 0.0;
                 for (int m = 0; m < L; ++m) {
-                    re += col[2 * m] * y[m];
-                    im += col[2 * m + 1] * y[m];
+                    // the reference build (g++ -O3, x86-64-v4) vectorises this in-order
+                    // reduction: products of m < n_unfused come from 8- and 4-wide vector
+                    // multiplies added one by one (acc + rnd(b y)); the last L mod 4 terms
+                    // run in the scalar epilogue as FMAs (acc = fma(b, y, acc))
+                    if (m < n_unfused) {
+                        re = __dadd_rn(re, __dmul_rn(col[2 * m], y[m]));
+                        im = __dadd_rn(im, __dmul_rn(col[2 * m + 1], y[m]));
+                    } else {
+                        re = __fma_rn(col[2 * m], y[m], re);
+                        im = __fma_rn(col[2 * m + 1], y[m], im);
+                    }
                 }
                 Rr[k] = re;
                 Ri[k] = im;
@@ -85,7 +99,8 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a,
                 for (int k = lane; k < K; k += 32) {
                     const double dk = ct.d64[k];
                     if (dk <= 0.0) continue;
-                    const double s = a.wc.q64[k] * (Rr[k] * Rr[k] + Ri[k] * Ri[k]) / dk;
+                    const double s = __ddiv_rn(
+                        __dmul_rn(a.wc.q64[k], __fma_rn(Rr[k], Rr[k], __dmul_rn(Ri[k], Ri[k]))), dk);
                     if (best < 0 || s > bs) {
                         best = k;
                         bs = s;
@@ -125,8 +140,8 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a,
                 const double* col = ct.c64 + size_t(u) * K * 2;
                 for (int s = lane; s < K; s += 32) {
                     const double c_r = col[2 * s], c_i = col[2 * s + 1];
-                    Rr[s] -= gr * c_r - gi * c_i;
-                    Ri[s] -= gr * c_i + gi * c_r;
+                    Rr[s] = __dsub_rn(Rr[s], __fma_rn(gr, c_r, -__dmul_rn(gi, c_i)));
+                    Ri[s] = __dsub_rn(Ri[s], __fma_rn(gr, c_i, __dmul_rn(gi, c_r)));
                 }
                 __syncwarp();
             }
@@ -139,7 +154,8 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a,
                 for (int t = 0; t < nactive; ++t) {
                     const int f = order[t];
                     const int idx = (eta * (f / W) + gam * (f % W)) % W;
-                    v += cr[f] * a.wc.unit64[2 * idx] - ci[f] * a.wc.unit64[2 * idx + 1];
+                    v = __dadd_rn(v, __fma_rn(cr[f], a.wc.unit64[2 * idx],
+                                              -__dmul_rn(ci[f], a.wc.unit64[2 * idx + 1])));
                 }
                 const int orow = tk.block_row + p / B, ocol = tk.block_col + p % B;
                 if (orow < a.out_rows && ocol < a.out_cols) {
@@ -156,7 +172,8 @@ __global__ void __launch_bounds__(kWarpsF64 * 32) k_solve_f64(const SolveArgs a,
                         for (int t = 0; t < nactive; ++t) {
                             const int f = order[t];
                             const int idx = (eta * (f / W) + gam * (f % W)) % W;
-                            v += cr[f] * a.wc.unit64[2 * idx] - ci[f] * a.wc.unit64[2 * idx + 1];
+                            v = __dadd_rn(v, __fma_rn(cr[f], a.wc.unit64[2 * idx],
+                                                      -__dmul_rn(ci[f], a.wc.unit64[2 * idx + 1])));
                         }
                         a.trace_window[p] = v;
                     }

@@ -112,9 +112,10 @@ __global__ void __launch_bounds__(256) k_gram(const ClassBuild* __restrict__ cls
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    // accRe += sRe*uRe + sIm*uIm; accIm += sIm*uRe - sRe*uIm (rljsde.cpp:86-89)
-                    ar[i][j] += sr[i] * ur[j] + sim[i] * uim[j];
-                    ai[i][j] += sim[i] * ur[j] - sr[i] * uim[j];
+                    // accRe += sRe*uRe + sIm*uIm; accIm += sIm*uRe - sRe*uIm (rljsde.cpp:86-89),
+                    // rounded like the reference build: acc + fma(a, b, c*d) per m
+                    ar[i][j] = __dadd_rn(ar[i][j], __fma_rn(sr[i], ur[j], __dmul_rn(sim[i], uim[j])));
+                    ai[i][j] = __dadd_rn(ai[i][j], __fma_rn(sim[i], ur[j], -__dmul_rn(sr[i], uim[j])));
                 }
         }
         __syncthreads();
