@@ -13,3 +13,12 @@ with tq.Plan(pat, tq.ReconstructionConfig(compute=tq.COMPUTE_FP64, clip_output=F
     plan.reconstruct(frame)
     r = plan.reconstruct(frame)
 print(f"fp64 mode {rows}x{rows} P={P}: {r.seconds:.4f} s = {rows * rows / 1e6 / r.seconds:.2f} MP/s")
+import time  # noqa: E402
+t = time.perf_counter()
+with tq.Plan(pat, tq.ReconstructionConfig(compute=tq.COMPUTE_FP64, clip_output=False)) as plan:
+    plan.reconstruct(frame)
+    t1 = time.perf_counter()
+    r = plan.reconstruct(frame)
+    t2 = time.perf_counter()
+print(f"  wall: first call {t1 - t:.2f} s, second call {t2 - t1:.3f} s (report.seconds {r.seconds:.3f}, "
+      f"blocks {r.blocks_processed})")
