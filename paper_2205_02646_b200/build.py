@@ -20,7 +20,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["tables.cu", "solve_f32.cu", "solve_f64.cu", "solve_ljsde.cu", "sensor.cu", "probe.cu"]
+CU = ["tables.cu", "solve_f32.cu", "solve_f64.cu", "solve_f64r.cu", "solve_ljsde.cu", "sensor.cu", "probe.cu"]
 CPP = ["plan.cpp", "io.cpp"]
 HEADERS = [os.path.join(CSRC, "tqsb_internal.hpp"), os.path.join(CSRC, "solve_common.cuh"),
            os.path.join(INCLUDE, "tqsb", "tqsb.h"),

@@ -656,9 +656,15 @@ SolveArgs base_args(tqsb_plan* p, Device* d) {
 
 int launch(tqsb_plan* p, Device* d, const SolveArgs& a, cudaStream_t s) {
     if (a.counter) CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
-    int rc = p->cfg.algorithm == TQSB_ALGO_LJSDE ? launch_solve_ljsde(a, s, d->num_sms)
-             : uses_f32(p->cfg)                    ? launch_solve_f32(a, p->wt.NS, s, d->num_sms)
-                                                   : launch_solve_f64(a, s, d->num_sms);
+    int rc;
+    if (p->cfg.algorithm == TQSB_ALGO_LJSDE) {
+        rc = launch_solve_ljsde(a, s, d->num_sms);
+    } else if (uses_f32(p->cfg)) {
+        rc = launch_solve_f32(a, p->wt.NS, s, d->num_sms);
+    } else {  // fp64 mode: register-resident kernel where it applies, else the general one
+        rc = launch_solve_f64r(a, s, d->num_sms);
+        if (rc == cudaErrorNotSupported) rc = launch_solve_f64(a, s, d->num_sms);
+    }
     if (rc != 0)
         return set_error(TQSB_ECUDA, std::string("solve launch: ") +
                                          cudaGetErrorString(cudaError_t(rc)));

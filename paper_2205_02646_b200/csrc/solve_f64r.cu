@@ -1,0 +1,229 @@
+// solve_f64r.cu -- the fp64 parity / exact-reproduction solve with the residual in
+// registers (W <= 32). Same arithmetic as solve_f64.cu (the reference build's rounding,
+// expression for expression: bitwise equal to tqs::reconstruct), laid out for the B200:
+//
+//   * one warp per block; lane j holds R_k for k = j + 32 i, i < NE, in registers
+//     (64 doubles per lane at W = 32), so the per-iteration selection scan and the column
+//     cascade are unrolled register code with independent loads in flight instead of
+//     shared-memory read-modify-write loops;
+//   * selection: per lane the strict '>' first maximum over its k ascending, then a warp
+//     reduction with ties to the smaller k (= the reference's scan from k = 0,
+//     rljsde.cpp:144-158);
+//   * the picked R_u from its owner lane (uniform register switch + SHFL);
+//   * coefficients (ModelCoefficients: += per pick, first-touch active list, basis.hpp:40-58)
+//     in a per-warp shared-memory list; synthesis over the kept B x B pixels at the end
+//     (basis.cpp:52-73 restricted, pipeline.cpp:157-166);
+//   * warps take blocks from a global counter (the class-sorted task list).
+// Tracing and windows above 32 use solve_f64.cu.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tqsb_internal.hpp"
+
+namespace tqsb {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kWarpsF64R = 8;
+
+struct F64RLayout {  // per-warp shared memory, in bytes
+    int K, nact_max, L_max;
+    __host__ __device__ size_t y_off() const { return 0; }
+    __host__ __device__ size_t re_off() const { return align(size_t(L_max) * 8); }
+    __host__ __device__ size_t im_off() const { return re_off() + align(size_t(nact_max) * 8); }
+    __host__ __device__ size_t f_off() const { return im_off() + align(size_t(nact_max) * 8); }
+    __host__ __device__ size_t idx_off() const { return f_off() + align(size_t(nact_max) * 4); }
+    __host__ __device__ size_t bytes() const { return idx_off() + align(size_t(K) * 2); }
+    __host__ __device__ static size_t align(size_t b) { return (b + 15) & ~size_t(15); }
+};
+
+// R[i] of this lane for a warp-uniform i (a uniform branch tree, no local memory)
+template <int NE>
+__device__ __forceinline__ double pick(const double (&R)[NE], int i) {
+    double v = 0.0;
+#pragma unroll
+    for (int n = 0; n < NE; ++n)
+        if (i == n) v = R[n];
+    return v;
+}
+
+template <int NE>
+__global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveArgs a, F64RLayout lay) {
+    extern __shared__ __align__(16) unsigned char smr[];
+    const int W = a.window, K = W * W, B = a.block;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* base = smr + size_t(warp) * lay.bytes();
+    double* y = reinterpret_cast<double*>(base + lay.y_off());
+    double* act_re = reinterpret_cast<double*>(base + lay.re_off());
+    double* act_im = reinterpret_cast<double*>(base + lay.im_off());
+    int* act_f = reinterpret_cast<int*>(base + lay.f_off());
+    short* idx_of = reinterpret_cast<short*>(base + lay.idx_off());
+    const double* __restrict__ q64 = a.wc.q64;
+    const double* __restrict__ unit = a.wc.unit64;
+
+    for (;;) {
+        int ti = 0;
+        if (lane == 0) ti = atomicAdd(a.counter, 1);
+        ti = __shfl_sync(FULL, ti, 0);
+        if (ti >= a.n_tasks) break;
+        const ClassTab ct = a.tabs[__ldg(a.task_cls + ti)];
+        const int L = ct.local;
+        const int n_unfused = 8 * (L / 8) + (L % 8 >= 4 ? 4 : 0);  // see solve_f64.cu
+        const Task tk = a.tasks[ti];
+        // gather_local_values (grid.cpp:104-114); pad_frame by clamping (pipeline.cpp:44-52)
+        {
+            const int r0 = (tk.origin_row + 1) / 2;
+            const int c0 = (tk.origin_col + 1) / 2, c1 = (tk.origin_col + W - 2) / 2;
+            const int ncol = c1 - c0 + 1;
+            for (int m = lane; m < L; m += 32) {
+                int fr = r0 + m / ncol, fc = c0 + m % ncol;
+                fr = fr < a.frame_rows - 1 ? fr : a.frame_rows - 1;
+                fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
+                y[m] = a.frame[size_t(fr - a.frame_row0) * a.frame_pitch + fc];
+            }
+            for (int k = lane; k < K; k += 32) idx_of[k] = -1;
+        }
+        __syncwarp();
+        // R = B y (rljsde.cpp:127-138) in the reference build's rounding
+        double Rr[NE], Ri[NE];
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const int k = lane + 32 * i;
+            double re = 0.0, im = 0.0;
+            if (k < K) {
+                const double2* col = reinterpret_cast<const double2*>(ct.b64) + size_t(k) * L;
+                for (int m = 0; m < L; ++m) {
+                    const double2 b = __ldg(col + m);
+                    if (m < n_unfused) {
+                        re = __dadd_rn(re, __dmul_rn(b.x, y[m]));
+                        im = __dadd_rn(im, __dmul_rn(b.y, y[m]));
+                    } else {
+                        re = __fma_rn(b.x, y[m], re);
+                        im = __fma_rn(b.y, y[m], im);
+                    }
+                }
+            }
+            Rr[i] = re;
+            Ri[i] = im;
+        }
+
+        int nact = 0;
+        for (int it = 0; it < a.iterations; ++it) {
+            // ---- selection: q |R|^2 / D, strict first maximum ----
+            int best = -1;
+            double bs = 0.0;
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                const int k = lane + 32 * i;
+                if (k < K) {
+                    const double dk = __ldg(ct.d64 + k);
+                    if (dk > 0.0) {
+                        const double s = __ddiv_rn(
+                            __dmul_rn(__ldg(q64 + k), __fma_rn(Rr[i], Rr[i], __dmul_rn(Ri[i], Ri[i]))), dk);
+                        if (best < 0 || s > bs) {
+                            best = k;
+                            bs = s;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double os = __shfl_xor_sync(FULL, bs, off);
+                const int ok = __shfl_xor_sync(FULL, best, off);
+                if (ok >= 0 && (best < 0 || os > bs || (os == bs && ok < best))) {
+                    bs = os;
+                    best = ok;
+                }
+            }
+            if (best < 0) break;  // no admissible frequency (rljsde.cpp:159)
+            const int u = best;
+            const double ur = __shfl_sync(FULL, pick<NE>(Rr, u >> 5), u & 31);
+            const double ui = __shfl_sync(FULL, pick<NE>(Ri, u >> 5), u & 31);
+            const double du = __ldg(ct.d64 + u);
+            const double gr = a.step * (ur / du), gi = a.step * (ui / du);
+            // ---- coefficients (ModelCoefficients::add, first-touch active list) ----
+            const int idx = idx_of[u];
+            __syncwarp();
+            if (lane == 0) {
+                if (idx < 0) {
+                    idx_of[u] = short(nact);
+                    act_f[nact] = u;
+                    act_re[nact] = gr;
+                    act_im[nact] = gi;
+                } else {
+                    act_re[idx] += gr;
+                    act_im[idx] += gi;
+                }
+            }
+            if (idx < 0) ++nact;
+            __syncwarp();  // lane 0's list writes are visible to the next iteration's reads
+            // ---- column cascade: R_s -= g C[s,u] (rljsde.cpp:160-172) ----
+            const double2* col = reinterpret_cast<const double2*>(ct.c64) + size_t(u) * K + lane;
+            constexpr int CH = NE < 8 ? NE : 8;
+#pragma unroll
+            for (int i0 = 0; i0 < NE; i0 += CH) {
+                double2 c[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    c[j] = (lane + 32 * (i0 + j) < K) ? __ldg(col + 32 * (i0 + j)) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int i = i0 + j;
+                    Rr[i] = __dsub_rn(Rr[i], __fma_rn(gr, c[j].x, -__dmul_rn(gi, c[j].y)));
+                    Ri[i] = __dsub_rn(Ri[i], __fma_rn(gr, c[j].y, __dmul_rn(gi, c[j].x)));
+                }
+            }
+        }
+        __syncwarp();
+        // ---- synthesize_real over the kept pixels (basis.cpp:52-73), place ----
+        const int rw = tk.block_row - tk.origin_row, cw = tk.block_col - tk.origin_col;
+        for (int p = lane; p < B * B; p += 32) {
+            const int eta = rw + p / B, gam = cw + p % B;
+            double v = 0.0;
+            for (int t = 0; t < nact; ++t) {
+                const int f = act_f[t];
+                const int ix = (eta * (f / W) + gam * (f % W)) % W;
+                v = __dadd_rn(v, __fma_rn(act_re[t], unit[2 * ix], -__dmul_rn(act_im[t], unit[2 * ix + 1])));
+            }
+            const int orow = tk.block_row + p / B, ocol = tk.block_col + p % B;
+            if (orow < a.out_rows && ocol < a.out_cols) {
+                if (a.clip) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+                a.out[size_t(orow - a.out_row0) * a.out_cols + ocol] = v;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int NE>
+int launch_ne(const SolveArgs& a, cudaStream_t st, int num_sms) {
+    const int K = a.window * a.window;
+    F64RLayout lay{K, a.iterations < K ? (a.iterations > 0 ? a.iterations : 1) : K, K / 4 + 1};
+    const size_t smem = lay.bytes() * kWarpsF64R;
+    cudaError_t e = cudaFuncSetAttribute(k_solve_f64r<NE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    k_solve_f64r<NE><<<num_sms, kWarpsF64R * 32, smem, st>>>(a, lay);
+    return cudaGetLastError();
+}
+
+} // namespace
+
+// fp64 mode for W <= 32 without tracing; returns cudaErrorNotSupported otherwise
+int launch_solve_f64r(const SolveArgs& a, void* stream, int num_sms) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int K = a.window * a.window;
+    if (a.window > 32 || a.trace_picks || !a.counter || !a.task_cls || force_global_state())
+        return cudaErrorNotSupported;
+    const int ne = (K + 31) / 32;
+    if (ne <= 1) return launch_ne<1>(a, st, num_sms);
+    if (ne <= 2) return launch_ne<2>(a, st, num_sms);
+    if (ne <= 4) return launch_ne<4>(a, st, num_sms);
+    if (ne <= 8) return launch_ne<8>(a, st, num_sms);
+    if (ne <= 16) return launch_ne<16>(a, st, num_sms);
+    return launch_ne<32>(a, st, num_sms);
+}
+
+} // namespace tqsb
