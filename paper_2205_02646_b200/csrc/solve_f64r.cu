@@ -26,6 +26,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kWarpsF64R = 8;
+constexpr int kTileM = 32;  // m columns of the shared B tile
 
 struct F64RLayout {  // per-warp shared memory, in bytes
     int K, nact_max, L_max;
@@ -62,15 +63,32 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
     const double* __restrict__ q64 = a.wc.q64;
     const double* __restrict__ unit = a.wc.unit64;
 
+    // the CTA takes kWarpsF64R consecutive tasks at a time (one per warp); when they share a
+    // class, the init R = B y streams the class's B through shared memory once for all of
+    // them (B: K x L complex = 4 MB at W = 32, otherwise re-read from L2 by every block)
+    double2* tile = reinterpret_cast<double2*>(smr + size_t(kWarpsF64R) * lay.bytes());
+    __shared__ int s_t0, s_cls0, s_same;
     for (;;) {
-        int ti = 0;
-        if (lane == 0) ti = atomicAdd(a.counter, 1);
-        ti = __shfl_sync(FULL, ti, 0);
-        if (ti >= a.n_tasks) break;
-        const ClassTab ct = a.tabs[__ldg(a.task_cls + ti)];
+        if (threadIdx.x == 0) s_t0 = atomicAdd(a.counter, kWarpsF64R);
+        __syncthreads();
+        const int t0 = s_t0;
+        if (t0 >= a.n_tasks) break;
+        const int ti = t0 + warp;
+        const bool active = ti < a.n_tasks;
+        const int my_cls = active ? __ldg(a.task_cls + ti) : -1;
+        if (threadIdx.x == 0) {
+            s_cls0 = my_cls;
+            s_same = 1;
+        }
+        __syncthreads();
+        if (lane == 0 && active && my_cls != s_cls0) s_same = 0;
+        __syncthreads();
+        const bool shared_init = s_same != 0;
+        const int cls = active ? my_cls : s_cls0;
+        const ClassTab ct = a.tabs[cls];
         const int L = ct.local;
         const int n_unfused = 8 * (L / 8) + (L % 8 >= 4 ? 4 : 0);  // see solve_f64.cu
-        const Task tk = a.tasks[ti];
+        const Task tk = active ? a.tasks[ti] : a.tasks[t0];
         // gather_local_values (grid.cpp:104-114); pad_frame by clamping (pipeline.cpp:44-52)
         {
             const int r0 = (tk.origin_row + 1) / 2;
@@ -85,27 +103,58 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
             for (int k = lane; k < K; k += 32) idx_of[k] = -1;
         }
         __syncwarp();
-        // R = B y (rljsde.cpp:127-138) in the reference build's rounding
+        // R = B y (rljsde.cpp:127-138) in the reference build's rounding, m ascending per k
         double Rr[NE], Ri[NE];
-#pragma unroll
-        for (int i = 0; i < NE; ++i) {
-            const int k = lane + 32 * i;
-            double re = 0.0, im = 0.0;
-            if (k < K) {
-                const double2* col = reinterpret_cast<const double2*>(ct.b64) + size_t(k) * L;
-                for (int m = 0; m < L; ++m) {
-                    const double2 b = __ldg(col + m);
-                    if (m < n_unfused) {
-                        re = __dadd_rn(re, __dmul_rn(b.x, y[m]));
-                        im = __dadd_rn(im, __dmul_rn(b.y, y[m]));
-                    } else {
-                        re = __fma_rn(b.x, y[m], re);
-                        im = __fma_rn(b.y, y[m], im);
-                    }
-                }
+        auto term = [&](double& re, double& im, double2 b, int m) {
+            if (m < n_unfused) {
+                re = __dadd_rn(re, __dmul_rn(b.x, y[m]));
+                im = __dadd_rn(im, __dmul_rn(b.y, y[m]));
+            } else {
+                re = __fma_rn(b.x, y[m], re);
+                im = __fma_rn(b.y, y[m], im);
             }
-            Rr[i] = re;
-            Ri[i] = im;
+        };
+        if (shared_init) {
+            const double2* bk = reinterpret_cast<const double2*>(ct.b64);
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                double re = 0.0, im = 0.0;
+                for (int m0 = 0; m0 < L; m0 += kTileM) {
+                    const int mc = L - m0 < kTileM ? L - m0 : kTileM;
+                    // rows k = 32 i .. 32 i + 31, columns m0 .. m0 + mc: one 512 B row piece
+                    // per warp load, padded row stride (kTileM + 1) double2: conflict-free reads
+                    for (int e = threadIdx.x; e < 32 * kTileM; e += kWarpsF64R * 32) {
+                        const int r = e / kTileM, mm = e % kTileM;
+                        const int k = 32 * i + r;
+                        tile[r * (kTileM + 1) + mm] =
+                            (k < K && mm < mc) ? __ldg(bk + size_t(k) * L + m0 + mm) : make_double2(0.0, 0.0);
+                    }
+                    __syncthreads();
+                    if (active && lane + 32 * i < K) {
+                        const double2* row = tile + lane * (kTileM + 1);
+                        for (int mm = 0; mm < mc; ++mm) term(re, im, row[mm], m0 + mm);
+                    }
+                    __syncthreads();
+                }
+                Rr[i] = re;
+                Ri[i] = im;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                const int k = lane + 32 * i;
+                double re = 0.0, im = 0.0;
+                if (k < K && active) {
+                    const double2* col = reinterpret_cast<const double2*>(ct.b64) + size_t(k) * L;
+                    for (int m = 0; m < L; ++m) term(re, im, __ldg(col + m), m);
+                }
+                Rr[i] = re;
+                Ri[i] = im;
+            }
+        }
+        if (!active) {  // a short last group: idle warps only joined the shared init
+            __syncthreads();
+            continue;
         }
 
         int nact = 0;
@@ -193,7 +242,7 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
                 a.out[size_t(orow - a.out_row0) * a.out_cols + ocol] = v;
             }
         }
-        __syncwarp();
+        __syncthreads();  // the group ends together (s_t0 and the tile are reused)
     }
 }
 
@@ -201,7 +250,7 @@ template <int NE>
 int launch_ne(const SolveArgs& a, cudaStream_t st, int num_sms) {
     const int K = a.window * a.window;
     F64RLayout lay{K, a.iterations < K ? (a.iterations > 0 ? a.iterations : 1) : K, K / 4 + 1};
-    const size_t smem = lay.bytes() * kWarpsF64R;
+    const size_t smem = lay.bytes() * kWarpsF64R + size_t(32) * (kTileM + 1) * sizeof(double2);
     cudaError_t e = cudaFuncSetAttribute(k_solve_f64r<NE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
