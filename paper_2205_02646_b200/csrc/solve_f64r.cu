@@ -35,18 +35,25 @@ struct F64RLayout {  // per-warp shared memory, in bytes
     __host__ __device__ size_t im_off() const { return re_off() + align(size_t(nact_max) * 8); }
     __host__ __device__ size_t f_off() const { return im_off() + align(size_t(nact_max) * 8); }
     __host__ __device__ size_t idx_off() const { return f_off() + align(size_t(nact_max) * 4); }
-    __host__ __device__ size_t bytes() const { return idx_off() + align(size_t(K) * 2); }
+    __host__ __device__ size_t d_off() const { return idx_off() + align(size_t(K) * 2); }
+    __host__ __device__ size_t bytes() const { return d_off() + align(size_t(K) * 8); }
     __host__ __device__ static size_t align(size_t b) { return (b + 15) & ~size_t(15); }
 };
 
-// R[i] of this lane for a warp-uniform i (a uniform branch tree, no local memory)
+// R[i] of this lane for a warp-uniform i: a binary branch tree over the register array
+// (log2 NE uniform branches, no local memory)
+template <int LO, int HI, int NE>
+__device__ __forceinline__ double pick_bs(const double (&R)[NE], int i) {
+    if constexpr (HI - LO == 1) {
+        return R[LO];
+    } else {
+        constexpr int MID = (LO + HI) / 2;
+        return i < MID ? pick_bs<LO, MID, NE>(R, i) : pick_bs<MID, HI, NE>(R, i);
+    }
+}
 template <int NE>
 __device__ __forceinline__ double pick(const double (&R)[NE], int i) {
-    double v = 0.0;
-#pragma unroll
-    for (int n = 0; n < NE; ++n)
-        if (i == n) v = R[n];
-    return v;
+    return pick_bs<0, NE, NE>(R, i);
 }
 
 template <int NE>
@@ -60,6 +67,7 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
     double* act_im = reinterpret_cast<double*>(base + lay.im_off());
     int* act_f = reinterpret_cast<int*>(base + lay.f_off());
     short* idx_of = reinterpret_cast<short*>(base + lay.idx_off());
+    double* dsm = reinterpret_cast<double*>(base + lay.d_off());  // the block's class D
     const double* __restrict__ q64 = a.wc.q64;
     const double* __restrict__ unit = a.wc.unit64;
 
@@ -67,6 +75,8 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
     // class, the init R = B y streams the class's B through shared memory once for all of
     // them (B: K x L complex = 4 MB at W = 32, otherwise re-read from L2 by every block)
     double2* tile = reinterpret_cast<double2*>(smr + size_t(kWarpsF64R) * lay.bytes());
+    double* qsm = reinterpret_cast<double*>(tile + 32 * (kTileM + 1));  // q (class independent)
+    for (int k = threadIdx.x; k < K; k += blockDim.x) qsm[k] = q64[k];
     __shared__ int s_t0, s_cls0, s_same;
     for (;;) {
         if (threadIdx.x == 0) s_t0 = atomicAdd(a.counter, kWarpsF64R);
@@ -100,7 +110,10 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
                 fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
                 y[m] = a.frame[size_t(fr - a.frame_row0) * a.frame_pitch + fc];
             }
-            for (int k = lane; k < K; k += 32) idx_of[k] = -1;
+            for (int k = lane; k < K; k += 32) {
+                idx_of[k] = -1;
+                dsm[k] = __ldg(ct.d64 + k);
+            }
         }
         __syncwarp();
         // R = B y (rljsde.cpp:127-138) in the reference build's rounding, m ascending per k
@@ -166,10 +179,10 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
             for (int i = 0; i < NE; ++i) {
                 const int k = lane + 32 * i;
                 if (k < K) {
-                    const double dk = __ldg(ct.d64 + k);
+                    const double dk = dsm[k];
                     if (dk > 0.0) {
                         const double s = __ddiv_rn(
-                            __dmul_rn(__ldg(q64 + k), __fma_rn(Rr[i], Rr[i], __dmul_rn(Ri[i], Ri[i]))), dk);
+                            __dmul_rn(qsm[k], __fma_rn(Rr[i], Rr[i], __dmul_rn(Ri[i], Ri[i]))), dk);
                         if (best < 0 || s > bs) {
                             best = k;
                             bs = s;
@@ -190,7 +203,7 @@ __global__ void __launch_bounds__(kWarpsF64R * 32, 1) k_solve_f64r(const SolveAr
             const int u = best;
             const double ur = __shfl_sync(FULL, pick<NE>(Rr, u >> 5), u & 31);
             const double ui = __shfl_sync(FULL, pick<NE>(Ri, u >> 5), u & 31);
-            const double du = __ldg(ct.d64 + u);
+            const double du = dsm[u];
             const double gr = a.step * (ur / du), gi = a.step * (ui / du);
             // ---- coefficients (ModelCoefficients::add, first-touch active list) ----
             const int idx = idx_of[u];
@@ -250,7 +263,8 @@ template <int NE>
 int launch_ne(const SolveArgs& a, cudaStream_t st, int num_sms) {
     const int K = a.window * a.window;
     F64RLayout lay{K, a.iterations < K ? (a.iterations > 0 ? a.iterations : 1) : K, K / 4 + 1};
-    const size_t smem = lay.bytes() * kWarpsF64R + size_t(32) * (kTileM + 1) * sizeof(double2);
+    const size_t smem = lay.bytes() * kWarpsF64R + size_t(32) * (kTileM + 1) * sizeof(double2) +
+                        size_t(K) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_solve_f64r<NE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
