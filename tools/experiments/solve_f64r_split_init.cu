@@ -5,6 +5,11 @@
 // 38 % slower (258 -> 356 ms) with no init code in the kernel, so the fused variants'
 // slowdown (solve_f64r_exchange_init.cu) is not register pressure from the init.
 // Net 12.96 -> 11.86 MP/s. profiles/r01_variants_fp64_init.jsonl; DESIGN.md section 5.
+// Variant 'splitgrp' (also bitwise, no faster: 11.75-12.02 MP/s): the solve loop's task fetch
+// replaced by a CTA group of 8 consecutive tasks, as in the committed kernel:
+//     __shared__ int grp_s;  for (;;) { __syncthreads(); if (threadIdx.x == 0) grp_s =
+//     atomicAdd(a.counter, kWarpsF64R); __syncthreads(); const int ti = grp_s + warp;
+//     if (grp_s >= a.n_tasks) break; if (ti >= a.n_tasks) continue; ... }
 // solve_f64r.cu -- the fp64 parity / exact-reproduction solve with the residual in
 // registers (W <= 32). Same arithmetic as solve_f64.cu (the reference build's rounding,
 // expression for expression: bitwise equal to tqs::reconstruct), laid out for the B200:
