@@ -15,8 +15,19 @@ with a 14 px halo, no collective on the data path).
   e2e    : the public C-ABI call with host buffers (tqsb_reconstruct_band on
            pinned host memory): H2D of the band's frame rows + solve + D2H of the
            band's output, host wall clock per step, max over ranks
+  e2e_pageable : the drop-in call exactly as a caller of tqs::reconstruct makes it
+           (tqsb_reconstruct on pageable numpy buffers, a fresh output per call)
+  parity : the timed output against the unmodified reference's full-frame run on
+           this host (outside the timed region): max-abs, dPSNR, px > 1e-4
+  cpu_baseline : the reference on the same frame -- a 128-row strip (the reference
+           arm's sample), the full frame (checks the strip extrapolation) and the
+           per-core figure (threads = 1, the paper's protocol)
   --impl reference : the unmodified reference (oracle/_ref, compiled from the
            reference sources) on this host's cores, same metric, bounded sample
+
+Multi-rank runs (torchrun) use NCCL when every rank has its own GPU and gloo when ranks
+share one (e.g. --nproc-per-node 2 on a 1-GPU box: exercises the band split and the
+bitwise reassembly of the frame; its timings are then not a scaling measurement).
 """
 from __future__ import annotations
 
@@ -103,10 +114,10 @@ def make_inputs(wl):
 
 
 # ---------------------------------------------------------------- CPU reference
-def run_reference_sample(wl, sample_rows, steps, warmup):
+def run_reference_sample(wl, sample_rows, steps, warmup, threads=0):
     """The unmodified reference on a strip of the workload (rows 0..sample_rows),
-    threads = hardware concurrency, shared kernel cache (warm excluded after the
-    first call, like the reference's own bench, pipeline.cpp:258-329)."""
+    threads = hardware concurrency (0) or as given, shared kernel cache (warm excluded
+    after the first call, like the reference's own bench, pipeline.cpp:258-329)."""
     import oracle
     ref = oracle.Reference()
     gt = ref.synthetic_image(wl["rows"], wl["cols"], wl["seed"])
@@ -119,7 +130,7 @@ def run_reference_sample(wl, sample_rows, steps, warmup):
     try:
         for i in range(warmup + steps):
             t0 = time.perf_counter()
-            _, rep = ref.reconstruct(strip, pat, wl["period"], threads=0, cache=cache)
+            _, rep = ref.reconstruct(strip, pat, wl["period"], threads=threads, cache=cache)
             wall = time.perf_counter() - t0
             if i >= warmup:
                 rates.append(mp / wall)
@@ -164,6 +175,24 @@ def main_reference(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_reference_full(wl, frame, opaque, clip=True):
+    """The unmodified reference on the whole workload frame, all host threads, warm
+    pass first (excluded like report.warmSeconds): the output for the parity line and
+    the full-frame rate that checks the strip extrapolation."""
+    import oracle
+    ref = oracle.Reference()
+    cache = ref.new_cache()
+    try:  # the warm pass runs inside the call; its time is reported apart and excluded
+        t0 = time.perf_counter()
+        out, rep = ref.reconstruct(frame, opaque, wl["period"], threads=0, cache=cache, clip=clip)
+        wall = time.perf_counter() - t0
+    finally:
+        ref.free_cache(cache)
+    mp = frame.shape[0] * frame.shape[1] * 4 / 1e6
+    return out, dict(value=mp / (wall - rep.warm_seconds), block_phase=mp / rep.seconds,
+                     wall_s=wall, warm_s=rep.warm_seconds, cores=rep.threads_used)
 
 
 # ---------------------------------------------------------------- clocks
@@ -219,14 +248,28 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- our arm
+def init_dist(world, local):
+    """One process per GPU: NCCL when every rank has its own GPU; gloo (CPU tensors)
+    when ranks share GPUs (a 1-GPU box running --nproc-per-node 2). Returns (dist,
+    device index, reduce device)."""
+    import torch
+    ndev = torch.cuda.device_count()
+    dev = local % max(1, ndev)
+    torch.cuda.set_device(dev)
+    if world <= 1:
+        return None, dev, f"cuda:{dev}"
+    import torch.distributed as dist
+    if world <= ndev:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        return dist, dev, f"cuda:{dev}"
+    dist.init_process_group("gloo")
+    return dist, dev, "cpu"
+
+
 def main_ours(args):
     import torch
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, local, red_dev = init_dist(world, local)
     import paper_2205_02646_b200 as tq
 
     wl = workload(args)
@@ -306,30 +349,80 @@ def main_ours(args):
     h2d = (f1 - f0) * fc * 8
     d2h = (out_r1 - out_r0) * N * 8
 
+    # ---- the drop-in exactly as a tqs::reconstruct caller makes it: pageable numpy
+    # buffers, a fresh output each call (the reference returns a new Image) ----
+    frame_pg = np.array(frame)  # pageable
+    pg_t = []
+    for i in range(max(1, args.warmup) + args.steps):
+        t = time.perf_counter()
+        if world == 1:
+            o = plan.reconstruct(frame_pg).output
+        else:
+            o = plan.reconstruct_band(frame_pg, br0, br1).output
+        if i >= max(1, args.warmup):
+            pg_t.append(time.perf_counter() - t)
+    pg_ms = statistics.mean(pg_t) * 1e3
+    ok_pg = bool(np.array_equal(o, h_out))
+
     # ---- max / sum over ranks ----
     vals = torch.tensor([mean_ms, e2e_ms, float(h2d), float(d2h), float(n_blocks),
-                         float(launches)], dtype=torch.float64, device=f"cuda:{local}")
+                         float(launches), pg_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         mx = vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = vals.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        mean_ms, e2e_ms = mx[0].item(), mx[1].item()
+        mean_ms, e2e_ms, pg_ms = mx[0].item(), mx[1].item(), mx[6].item()
         h2d, d2h, tot_blocks, tot_launch = sm[2].item(), sm[3].item(), sm[4].item(), sm[5].item()
     else:
         tot_blocks, tot_launch = float(n_blocks), float(launches)
+
+    # ---- the timed frame, reassembled on rank 0 (outside every timed region) ----
+    full = None
+    bands_bitwise = None
+    band_out = d_out.cpu().numpy()
+    if world > 1:
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object(band_out, parts, dst=0)
+        if rank == 0:
+            full = np.concatenate(parts)
+            one = plan.reconstruct(frame).output  # the whole frame on one device
+            bands_bitwise = bool(full.tobytes() == one.tobytes())
+    else:
+        full = band_out
     mp = M * N / 1e6
     value = mp / (mean_ms * 1e-3)
     e2e_value = mp / (e2e_ms * 1e-3)
     kernel_tflops = F_BLOCK * n_blocks / (statistics.mean(step_ms) * 1e-3) / 1e12
 
     nominal_mhz = (clk or {}).get("sm_max_mhz") or 1965.0
+    peak_nominal = NOMINAL_FMA_PER_CLK * 2 * nominal_mhz * 1e6 / 1e12
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    parity = None
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            r = run_reference_sample(wl, args.cpu_sample_rows, 2, 1)
+            r = run_reference_sample(wl, args.cpu_sample_rows, 3, 1)
             cpu = {"value": round(r["value"], 5), "unit": "MP/s", "cores": r["cores"],
                    "kind": "reference", "sample": r["sample"], "cpu": cpu_model()}
+            # full frame: the parity reference and a check of the strip extrapolation
+            want, rf = run_reference_full(wl, frame, pat.opaque, clip=True)
+            cpu["full_frame_value"] = round(rf["value"], 5)
+            cpu["full_frame_seconds"] = round(rf["wall_s"] - rf["warm_s"], 2)
+            cpu["full_frame_warm_seconds"] = round(rf["warm_s"], 2)
+            cpu["strip_vs_full"] = round(r["value"] / rf["value"], 4)
+            d = np.abs(full - want)
+            p_ours = 10 * np.log10(1.0 / np.mean((gt - full) ** 2))
+            p_ref = 10 * np.log10(1.0 / np.mean((gt - want) ** 2))
+            parity = {"vs": "unmodified reference, full frame, fp64, clip on (as timed)",
+                      "max_abs": float(d.max()), "dpsnr_db": round(float(p_ours - p_ref), 7),
+                      "psnr_db": round(float(p_ours), 4), "psnr_ref_db": round(float(p_ref), 4),
+                      "px_gt_1e4": int((d > 1e-4).sum()), "px": int(d.size),
+                      "gate": "max_abs <= 1e-2 and |dpsnr| <= 0.01 dB",
+                      "pass": bool(d.max() <= 1e-2 and abs(p_ours - p_ref) <= 0.01)}
+            # per core (threads = 1): the paper's protocol, on a 16-row strip
+            r1 = run_reference_sample(wl, 16, 1, 1, threads=1)
+            cpu["per_core_value"] = round(r1["value"], 6)
+            cpu["per_core_sample"] = r1["sample"] + ", threads = 1"
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "MP/s", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -353,27 +446,38 @@ def main_ours(args):
             "config": {"workload": wl["name"], "image_hw": [M, N], "period_px": wl["period"],
                        "window": W, "block": B, "iterations": cfg.max_iterations,
                        "step_width": cfg.step_width, "clip": True, "compute": "fp32",
-                       "parallelism": f"row bands x{world}", "blocks": int(tot_blocks),
+                       "parallelism": f"row bands x{world}" + (
+                           "" if red_dev != "cpu" else " (ranks share one GPU, gloo)"),
+                       "blocks": int(tot_blocks),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "hot_columns": "auto (0: TMEM tier off)"},
             "e2e": {"value": round(e2e_value, 3), "unit": "MP/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": round(e2e_ms, 3), "matches_device_output": ok_e2e},
+                    "ms_per_step": round(e2e_ms, 3), "matches_device_output": ok_e2e,
+                    "buffers": "pinned host (tqsb_host_alloc), tqsb_reconstruct_band"},
+            "e2e_pageable": {"value": round(mp / (pg_ms * 1e-3), 3), "unit": "MP/s",
+                             "ms_per_step": round(pg_ms, 3), "matches_device_output": ok_pg,
+                             "buffers": "pageable numpy, fresh output per call "
+                                        "(tqsb_reconstruct: the tqs::reconstruct drop-in)"},
+            "parity": parity,
             "roofline": {"bound": "fp32", "achieved": round(kernel_tflops, 3),
-                         "peak": round(peaks["fp32_tflops"], 2), "unit": "TFLOP/s",
-                         "frac": round(kernel_tflops / peaks["fp32_tflops"], 4),
+                         "peak": round(peak_nominal, 2), "unit": "TFLOP/s",
+                         "frac": round(kernel_tflops / peak_nominal, 4),
                          "traffic": traffic,
                          "kernel": "k_solve_f32 (fused init/greedy loop/synthesis)",
                          "algorithmic": f"{F_BLOCK} flop/block x {n_blocks} blocks/launch",
-                         "peak_source": "measured this run: FFMA2 probe (tqsb_probe_peaks); "
+                         "peak_source": "nominal FP32 pipe: 148 SMs x 128 FMA/clk x 2 flop at "
+                                        f"{nominal_mhz:.0f} MHz (the sampled max SM clock); "
                                         "MEASURED_PEAKS.json has no FP32 figure",
+                         "peak_probe": round(peaks["fp32_tflops"], 2),
+                         "probe_frac_of_nominal": round(peaks["fp32_tflops"] / peak_nominal, 4),
+                         "frac_of_probe": round(kernel_tflops / peaks["fp32_tflops"], 4),
                          "smem_tbps_measured": round(peaks["smem_tbps"], 2),
-                         # nominal FP32 pipe: 148 SMs x 128 FMA/clk x 2 flop at the sampled clock
-                         "peak_nominal": round(NOMINAL_FMA_PER_CLK * 2 * nominal_mhz * 1e6 / 1e12, 2),
-                         "frac_nominal": round(kernel_tflops / (NOMINAL_FMA_PER_CLK * 2 * nominal_mhz
-                                                                * 1e6 / 1e12), 4),
-                         "executed_flop_per_block": EXEC_FLOP_BLOCK},
+                         "executed_flop_per_block": EXEC_FLOP_BLOCK,
+                         "executed_frac": round(EXEC_FLOP_BLOCK * n_blocks / (mean_ms * 1e-3)
+                                                / 1e12 / peak_nominal, 4)},
             "cpu_baseline": cpu,
+            "bands_reassembled_bitwise": bands_bitwise,
             "clocks": clk,
             "gpu_launches": int(tot_launch),
             "warm_seconds": round(warm_s, 3),
@@ -390,11 +494,7 @@ def main_video(args):
     import ctypes
     import torch
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, local, red_dev = init_dist(world, local)
     import paper_2205_02646_b200 as tq
     wl = workload(args)
     nf = wl["frames"]
@@ -495,7 +595,7 @@ def main_video(args):
         ds_ms.append(a.elapsed_time(b))
     ds_mean = statistics.mean(ds_ms)
     vals = torch.tensor([mean_ms, e2e_ms, float(len(frames) * in_b), float(len(frames) * out_b),
-                         float(launches), ds_mean], dtype=torch.float64, device=dev)
+                         float(launches), ds_mean], dtype=torch.float64, device=red_dev)
     if world > 1:
         mx, sm = vals.clone(), vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -505,6 +605,7 @@ def main_video(args):
     else:
         h2d, d2h, tot_launch = vals[2].item(), vals[3].item(), vals[4].item()
     mp = nf * M * N / 1e6
+    peak_nominal = NOMINAL_FMA_PER_CLK * 2 * ((clk or {}).get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
     kernel_tflops = F_BLOCK * blocks_per_frame * len(frames) / (statistics.mean(step_ms) * 1e-3) / 1e12
     if rank == 0:
         print(json.dumps({
@@ -521,8 +622,10 @@ def main_video(args):
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": round(e2e_ms, 3), "matches_device_output": ok},
             "roofline": {"bound": "fp32", "achieved": round(kernel_tflops, 3),
-                         "peak": round(peaks["fp32_tflops"], 2), "unit": "TFLOP/s",
-                         "frac": round(kernel_tflops / peaks["fp32_tflops"], 4), "traffic": None},
+                         "peak": round(peak_nominal, 2), "unit": "TFLOP/s",
+                         "frac": round(kernel_tflops / peak_nominal, 4), "traffic": None,
+                         "peak_source": "nominal FP32 pipe at the sampled max SM clock",
+                         "peak_probe": round(peaks["fp32_tflops"], 2)},
             "device_stream": {"value": round(mp / (ds_mean * 1e-3), 3), "unit": "MP/s",
                               "ms_per_step": round(ds_mean, 3),
                               "includes": "synthetic scene + sensor readout + reconstruction, "

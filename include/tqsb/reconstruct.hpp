@@ -12,13 +12,18 @@
 // (validation, pipeline.cpp:27-42), std::logic_error (cache window mismatch,
 // pipeline.cpp:146-147), std::runtime_error (device failures).
 //
-// KernelCache is the device-resident table store: bound to the first pattern and
-// config it sees, reused across calls (the reference's shared KernelCache,
-// pipeline.cpp:110-133), with hits()/misses() counters.
+// KernelCache is the device-resident table store (the reference's shared KernelCache,
+// pipeline.cpp:110-133, rljsde.hpp:81-100): it holds the fp64 B, C, D tables per
+// offset class on the GPU, bound to the window (and pattern) of its first use, with
+// hits()/misses() counters. Every call through it runs with that call's own config --
+// nu, gamma, block, clip, frequency exponent and compute -- like the reference's.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <limits>
+#include <numeric>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -104,6 +109,7 @@ struct ReconstructionReport {
     uint64_t cacheMisses = 0;
     std::optional<double> psnrDb;
     double e2eSeconds = 0.0;
+    Compute compute = Compute::Fp32;  // the arithmetic the call ran in (tqsb_report::compute)
 };
 
 namespace detail {
@@ -162,6 +168,7 @@ public:
     }
 
     // internal: bind on first use; a different window is the reference's logic_error
+    // (pipeline.cpp:146-147). The config's solver options are per call, not bound.
     tqsb_plan* bind(const QuadrantPattern& p, const ReconstructionConfig& c) {
         if (plan_) {
             if (window_ != c.window)
@@ -194,16 +201,18 @@ inline ReconstructionReport reconstruct(const MeasurementFrame& frame, const Qua
     if (frame.rows < 1 || frame.cols < 1) throw std::invalid_argument("empty measurement frame");
     if (reference && (reference->rows != 2 * frame.rows || reference->cols != 2 * frame.cols))
         throw std::invalid_argument("reference dimensions do not match the reconstruction");
-    // the reference shares its cache with RL-JSDE only (pipeline.cpp:111-112)
+    // the reference shares its cache with RL-JSDE only (pipeline.cpp:111-112): an
+    // L-JSDE call leaves a caller's cache untouched
     KernelCache local;
     KernelCache* kc = cache && config.algorithm == Algorithm::Rljsde ? cache : &local;
     tqsb_plan* plan = kc->bind(pattern, config);
     ReconstructionReport rep;
     rep.output = Image(2 * frame.rows, 2 * frame.cols);
     tqsb_report r;
-    detail::check(tqsb_reconstruct(plan, frame.values.data(), frame.rows, frame.cols,
-                                   rep.output.values.data(),
-                                   reference ? reference->values.data() : nullptr, &r));
+    detail::check(tqsb_reconstruct_with(plan, &k, frame.values.data(), frame.rows, frame.cols,
+                                        rep.output.values.data(),
+                                        reference ? reference->values.data() : nullptr, &r));
+    rep.compute = r.compute == TQSB_COMPUTE_FP64 ? Compute::Fp64 : Compute::Fp32;
     rep.seconds = r.seconds;
     rep.warmSeconds = r.warm_seconds;
     rep.e2eSeconds = r.e2e_seconds;
@@ -214,8 +223,171 @@ inline ReconstructionReport reconstruct(const MeasurementFrame& frame, const Qua
     rep.cacheHits = uint64_t(r.cache_hits);
     rep.cacheMisses = uint64_t(r.cache_misses);
     if (r.has_psnr) rep.psnrDb = r.psnr_db;
+    if (config.algorithm == Algorithm::Ljsde) {  // no cache, no counters (pipeline.cpp:173-177)
+        rep.cacheHits = rep.cacheMisses = 0;
+        rep.classesCreated = 0;
+    }
     kc->count(rep.cacheHits, rep.cacheMisses);
     return rep;
+}
+
+// ---- pipeline.hpp:49-64 helpers (pipeline.cpp:187-256) ----
+struct PaddedImage {
+    Image image;
+    int originalRows = 0;
+    int originalCols = 0;
+};
+
+// edge-replication padding to even, block-multiple dimensions (pipeline.cpp:187-209)
+inline PaddedImage pad_to_block_multiple(const Image& image, int block) {
+    if (block < 1) throw std::invalid_argument("block size must be positive");
+    if (image.rows < 1 || image.cols < 1) throw std::invalid_argument("empty image");
+    const int step = std::lcm(block, 2);
+    PaddedImage out;
+    out.originalRows = image.rows;
+    out.originalCols = image.cols;
+    const int rows = (image.rows + step - 1) / step * step, cols = (image.cols + step - 1) / step * step;
+    if (rows == image.rows && cols == image.cols) {
+        out.image = image;
+        return out;
+    }
+    out.image = Image(rows, cols);
+    for (int r = 0; r < rows; ++r) {
+        const double* src = &image.values[size_t(std::min(r, image.rows - 1)) * image.cols];
+        double* dst = &out.image.values[size_t(r) * cols];
+        std::copy(src, src + image.cols, dst);
+        std::fill(dst + image.cols, dst + cols, src[image.cols - 1]);
+    }
+    return out;
+}
+
+// top-left rows x cols (pipeline.cpp:211-219)
+inline Image crop_image(const Image& image, int rows, int cols) {
+    if (rows < 0 || cols < 0 || rows > image.rows || cols > image.cols)
+        throw std::invalid_argument("crop exceeds image bounds");
+    Image out(rows, cols);
+    for (int r = 0; r < rows; ++r)
+        std::copy_n(&image.values[size_t(r) * image.cols], cols, &out.values[size_t(r) * cols]);
+    return out;
+}
+
+// each measurement value copied to its 2x2 cell, the quality baseline (pipeline.cpp:235-246)
+inline Image nn_upsample(const MeasurementFrame& frame) {
+    Image out(2 * frame.rows, 2 * frame.cols);
+    for (int r = 0; r < frame.rows; ++r)
+        for (int c = 0; c < frame.cols; ++c) {
+            const double v = frame.at(r, c);
+            out.at(2 * r, 2 * c) = v;
+            out.at(2 * r, 2 * c + 1) = v;
+            out.at(2 * r + 1, 2 * c) = v;
+            out.at(2 * r + 1, 2 * c + 1) = v;
+        }
+    return out;
+}
+
+inline MeasurementFrame simulate_measurement(const Image& image, const QuadrantPattern& pattern);
+inline double psnr(const Image& reference, const Image& estimate);
+
+// simulate + reconstruct + PSNR against the unpadded input (pipeline.cpp:248-256): the
+// acceptance and benchmark call shape
+inline ReconstructionReport reconstruct_image(const Image& image, const QuadrantPattern& pattern,
+                                              const ReconstructionConfig& config,
+                                              KernelCache* cache = nullptr) {
+    PaddedImage padded = pad_to_block_multiple(image, config.block);
+    MeasurementFrame frame = simulate_measurement(padded.image, pattern);
+    ReconstructionReport report = reconstruct(frame, pattern, config, cache);
+    report.output = crop_image(report.output, padded.originalRows, padded.originalCols);
+    report.psnrDb = psnr(image, report.output);
+    return report;
+}
+
+// ---- bench (pipeline.hpp:78-100, pipeline.cpp:258-329) ----
+struct BenchResult {
+    int images = 0;
+    double ljsdeMeanSeconds = 0.0;
+    double rljsdeMeanSeconds = 0.0;      // excluding table precompute
+    double rljsdeMeanWarmSeconds = 0.0;  // precompute, averaged over runs
+    double speedup = 0.0;                // ljsde / rljsde (excl. precompute)
+    double speedupInclWarm = 0.0;
+    double maxAbsDifference = 0.0;       // worst pixel deviation across the set
+    bool scalingMeasured = false;        // per-block times at W=16 vs the config's window
+    double ljsdePerBlockSmall = 0.0, ljsdePerBlockLarge = 0.0;
+    double rljsdePerBlockSmall = 0.0, rljsdePerBlockLarge = 0.0;
+    double ljsdeScalingRatio = 0.0;
+    double rljsdeScalingRatio = 0.0;
+};
+
+// thrown when the two algorithms diverge beyond the threshold (pipeline.hpp:94-97)
+class EquivalenceError : public std::runtime_error {
+public:
+    EquivalenceError(const std::string& what, double maxAbs)
+        : std::runtime_error(what), maxAbsDifference(maxAbs) {}
+    double maxAbsDifference;
+};
+
+// L-JSDE vs RL-JSDE on the same frames, both on the device: L-JSDE always runs in
+// fp64; RL-JSDE in the config's compute (Compute::Fp64 reproduces the reference's
+// arithmetic and meets its 1e-6 bar; the fp32 product path meets the product tolerance).
+inline BenchResult bench(const std::vector<Image>& images, const QuadrantPattern& pattern,
+                         const ReconstructionConfig& config, double equivalenceThreshold = 1e-6,
+                         bool measureScaling = false) {
+    if (images.empty()) throw std::invalid_argument("bench requires at least one image");
+    ReconstructionConfig cfgL = config;
+    cfgL.algorithm = Algorithm::Ljsde;
+    cfgL.threads = 1;
+    cfgL.clipOutput = false;
+    ReconstructionConfig cfgR = cfgL;
+    cfgR.algorithm = Algorithm::Rljsde;
+    BenchResult result;
+    result.images = int(images.size());
+    KernelCache cache;
+    double sumL = 0.0, sumR = 0.0, sumWarm = 0.0;
+    for (const Image& image : images) {
+        PaddedImage padded = pad_to_block_multiple(image, config.block);
+        MeasurementFrame frame = simulate_measurement(padded.image, pattern);
+        ReconstructionReport runL = reconstruct(frame, pattern, cfgL);
+        ReconstructionReport runR = reconstruct(frame, pattern, cfgR, &cache);
+        sumL += runL.seconds;
+        sumR += runR.seconds;
+        sumWarm += runR.warmSeconds;
+        for (size_t i = 0; i < runL.output.size(); ++i)
+            result.maxAbsDifference = std::max(
+                result.maxAbsDifference, std::abs(runL.output.values[i] - runR.output.values[i]));
+    }
+    result.ljsdeMeanSeconds = sumL / result.images;
+    result.rljsdeMeanSeconds = sumR / result.images;
+    result.rljsdeMeanWarmSeconds = sumWarm / result.images;
+    result.speedup = result.rljsdeMeanSeconds > 0.0 ? result.ljsdeMeanSeconds / result.rljsdeMeanSeconds
+                                                    : std::numeric_limits<double>::infinity();
+    const double inclusive = result.rljsdeMeanSeconds + result.rljsdeMeanWarmSeconds;
+    result.speedupInclWarm = inclusive > 0.0 ? result.ljsdeMeanSeconds / inclusive
+                                             : std::numeric_limits<double>::infinity();
+    if (result.maxAbsDifference > equivalenceThreshold)
+        throw EquivalenceError("algorithms diverged: max abs difference " +
+                                   std::to_string(result.maxAbsDifference) + " exceeds " +
+                                   std::to_string(equivalenceThreshold),
+                               result.maxAbsDifference);
+    if (measureScaling) {
+        PaddedImage padded = pad_to_block_multiple(images.front(), config.block);
+        MeasurementFrame frame = simulate_measurement(padded.image, pattern);
+        auto perBlock = [&](Algorithm algo, int window, double& out) {
+            ReconstructionConfig cfg = cfgL;
+            cfg.algorithm = algo;
+            cfg.window = window;
+            KernelCache scalingCache;  // tables are window-specific
+            ReconstructionReport run =
+                reconstruct(frame, pattern, cfg, algo == Algorithm::Rljsde ? &scalingCache : nullptr);
+            out = run.seconds / double(run.blocksProcessed);
+        };
+        perBlock(Algorithm::Ljsde, 16, result.ljsdePerBlockSmall);
+        perBlock(Algorithm::Ljsde, config.window, result.ljsdePerBlockLarge);
+        perBlock(Algorithm::Rljsde, 16, result.rljsdePerBlockSmall);
+        perBlock(Algorithm::Rljsde, config.window, result.rljsdePerBlockLarge);
+        result.ljsdeScalingRatio = result.ljsdePerBlockLarge / result.ljsdePerBlockSmall;
+        result.rljsdeScalingRatio = result.rljsdePerBlockLarge / result.rljsdePerBlockSmall;
+        result.scalingMeasured = true;
+    }
+    return result;
 }
 
 // ---- kernel-cache persistence and accounting (rljsde.hpp:102-131) ----

@@ -87,6 +87,9 @@ typedef struct tqsb_report {
     double psnr_db;            /* vs reference when supplied; +inf when identical */
     int has_psnr;
     int gpu_launches;          /* kernels launched by this call */
+    int compute;               /* TQSB_COMPUTE_* the call actually ran in: FP32 = the product
+                                  kernel; FP64 = the reference's fp64 arithmetic (compute=fp64,
+                                  L-JSDE, or W > 32 / B > 16, outside the fp32 kernel) */
 } tqsb_report;
 
 typedef struct tqsb_plan tqsb_plan;
@@ -107,8 +110,20 @@ int tqsb_census(int frame_rows, int frame_cols, const tqsb_config* cfg, int peri
 
 /* Plan: validates like pipeline.cpp:27-42 and binds the pattern
  * (opaque = (period/2)^2 quadrant indices, grid.hpp:19-34) to `n_devices`
- * CUDA devices. Tables are built lazily per offset class on first use and stay
- * resident (per device, replicated). devices = NULL uses 0..n_devices-1. */
+ * CUDA devices. The plan is the reference's KernelCache: the fp64 B, C, D tables of
+ * each offset class are built on first use and stay resident (per device,
+ * replicated), and nothing else is pinned by them. `cfg` is the default per-call
+ * configuration; the *_with entry points take the configuration per call instead
+ * (max_iterations, step_width, frequency_exponent, block, clip_output, compute,
+ * algorithm and early stop may differ from call to call; the fp32 product tables of
+ * each (frequency_exponent, step_width) are derived from the cached planes on first
+ * use). Like the reference's cache, which is keyed by offset class only, classes
+ * already resident are reused as built (spatial_decay and precision of the call that
+ * created them); a call with a different window fails with TQSB_ELOGIC
+ * ("kernel cache holds a different window size", pipeline.cpp:146-147).
+ * devices = NULL uses 0..n_devices-1; a device may be listed more than once (each
+ * entry is an independent context with its own streams, e.g. to exercise the
+ * multi-device band split on one GPU). */
 int tqsb_plan_create(const uint8_t* opaque, int period, const tqsb_config* cfg,
                      const int* devices, int n_devices, tqsb_plan** out);
 int tqsb_plan_destroy(tqsb_plan* plan);
@@ -120,6 +135,11 @@ int tqsb_plan_destroy(tqsb_plan* plan);
  * across the plan's devices in block-row bands. */
 int tqsb_reconstruct(tqsb_plan* plan, const double* frame, int frame_rows, int frame_cols,
                      double* out, const double* reference, tqsb_report* rep);
+/* The same with a per-call configuration (NULL = the plan's): the drop-in for
+ * tqs::reconstruct(frame, pattern, config, &cache, reference), pipeline.hpp:45-47. */
+int tqsb_reconstruct_with(tqsb_plan* plan, const tqsb_config* config, const double* frame,
+                          int frame_rows, int frame_cols, double* out, const double* reference,
+                          tqsb_report* rep);
 
 /* Band form (one process per GPU): reconstruct only output block rows
  * [block_row_begin, block_row_end) of the padded image on the plan's first
@@ -129,6 +149,9 @@ int tqsb_reconstruct(tqsb_plan* plan, const double* frame, int frame_rows, int f
 int tqsb_reconstruct_band(tqsb_plan* plan, const double* frame, int frame_rows, int frame_cols,
                           int block_row_begin, int block_row_end, double* out_band,
                           tqsb_report* rep);
+int tqsb_reconstruct_band_with(tqsb_plan* plan, const tqsb_config* config, const double* frame,
+                               int frame_rows, int frame_cols, int block_row_begin,
+                               int block_row_end, double* out_band, tqsb_report* rep);
 
 /* Multi-frame form (a video stream): n_frames frames of identical shape, frames[i]
  * and outs[i] host pointers (pinned buffers are used in place; pageable ones are
@@ -138,14 +161,22 @@ int tqsb_reconstruct_band(tqsb_plan* plan, const double* frame, int frame_rows, 
  * frames; rep->seconds is the device span of the batch (max over devices). */
 int tqsb_reconstruct_batch(tqsb_plan* plan, const double* const* frames, int n_frames,
                            int frame_rows, int frame_cols, double* const* outs, tqsb_report* rep);
+int tqsb_reconstruct_batch_with(tqsb_plan* plan, const tqsb_config* config,
+                                const double* const* frames, int n_frames, int frame_rows,
+                                int frame_cols, double* const* outs, tqsb_report* rep);
 
 /* Device-resident form on the plan's first device: d_frame / d_out are device
  * pointers (same layouts as tqsb_reconstruct), stream a cudaStream_t (NULL =
  * legacy default). Asynchronous: returns after enqueueing; rep->seconds is 0.
  * Tables for the frame's classes must be resident (tqsb_plan_warm) or are
- * built synchronously first. */
+ * built synchronously first. Every launch takes its own task-queue head from a
+ * ring of 64 (zeroed on the launch stream), so up to 64 reconstructions may be in
+ * flight on different streams at once. */
 int tqsb_reconstruct_device(tqsb_plan* plan, const double* d_frame, int frame_rows,
                             int frame_cols, double* d_out, void* stream, tqsb_report* rep);
+int tqsb_reconstruct_device_with(tqsb_plan* plan, const tqsb_config* config, const double* d_frame,
+                                 int frame_rows, int frame_cols, double* d_out, void* stream,
+                                 tqsb_report* rep);
 
 /* Band form of the device-resident entry point (rows as tqsb_reconstruct_band;
  * d_frame is the full frame in device memory, d_out_band the band). */

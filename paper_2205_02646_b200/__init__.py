@@ -62,7 +62,7 @@ class _Report(C.Structure):
                 ("classes_total", C.c_longlong), ("classes_interior", C.c_longlong),
                 ("classes_created", C.c_longlong), ("cache_hits", C.c_longlong),
                 ("cache_misses", C.c_longlong), ("psnr_db", C.c_double), ("has_psnr", C.c_int),
-                ("gpu_launches", C.c_int)]
+                ("gpu_launches", C.c_int), ("compute", C.c_int)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -80,7 +80,8 @@ EXPORTS = [
     "tqsb_io_read", "tqsb_io_write_pgm", "tqsb_io_write_tqsm", "tqsb_io_read_pattern",
     "tqsb_io_write_pattern", "tqsb_plan_save_tables", "tqsb_plan_load_tables",
     "tqsb_pattern_digest", "tqsb_kernel_memory_report", "tqsb_synthetic_image_device",
-    "tqsb_plan_simulate_device",
+    "tqsb_plan_simulate_device", "tqsb_reconstruct_with", "tqsb_reconstruct_batch_with",
+    "tqsb_reconstruct_band_with", "tqsb_reconstruct_device_with",
 ]
 
 
@@ -104,6 +105,16 @@ def _load() -> C.CDLL:
                                    C.POINTER(_Report)]
     L.tqsb_reconstruct_band.argtypes = [C.c_void_p, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
                                         _dp, C.POINTER(_Report)]
+    L.tqsb_reconstruct_with.argtypes = [C.c_void_p, C.POINTER(_Config), _dp, C.c_int, C.c_int,
+                                        _dp, _dp, C.POINTER(_Report)]
+    L.tqsb_reconstruct_band_with.argtypes = [C.c_void_p, C.POINTER(_Config), _dp, C.c_int,
+                                             C.c_int, C.c_int, C.c_int, _dp, C.POINTER(_Report)]
+    L.tqsb_reconstruct_batch_with.argtypes = [C.c_void_p, C.POINTER(_Config), C.POINTER(_dp),
+                                              C.c_int, C.c_int, C.c_int, C.POINTER(_dp),
+                                              C.POINTER(_Report)]
+    L.tqsb_reconstruct_device_with.argtypes = [C.c_void_p, C.POINTER(_Config), C.c_void_p,
+                                               C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                               C.POINTER(_Report)]
     L.tqsb_reconstruct_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
                                           C.c_void_p, C.POINTER(_Report)]
     L.tqsb_reconstruct_band_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
@@ -167,6 +178,18 @@ def _d(a: np.ndarray):
     return a.ctypes.data_as(_dp)
 
 
+def _out_array(out, shape, what="out"):
+    """A caller-supplied output buffer: the kernels and staging copies store straight
+    into it, so it must be exactly a C-contiguous float64 array of the output shape."""
+    if out is None:
+        return np.empty(shape)
+    if not isinstance(out, np.ndarray) or out.dtype != np.float64 or \
+            not out.flags.c_contiguous or not out.flags.writeable or tuple(out.shape) != tuple(shape):
+        raise ValueError(f"{what} must be a writeable C-contiguous float64 array of shape "
+                         f"{tuple(shape)}")
+    return out
+
+
 COMPUTE_FP32, COMPUTE_FP64 = 0, 1
 PRECISION_SINGLE, PRECISION_DOUBLE = 0, 1
 ALGO_LJSDE, ALGO_RLJSDE = 0, 1
@@ -212,13 +235,14 @@ class ReconstructionReport:
     cache_misses: int
     psnr_db: float | None
     gpu_launches: int
+    compute: int = 0  # COMPUTE_* the call actually ran in
 
 
 def _report(out, r: _Report) -> ReconstructionReport:
     return ReconstructionReport(out, r.seconds, r.warm_seconds, r.e2e_seconds, r.blocks_processed,
                                 r.classes_total, r.classes_interior, r.classes_created,
                                 r.cache_hits, r.cache_misses,
-                                r.psnr_db if r.has_psnr else None, r.gpu_launches)
+                                r.psnr_db if r.has_psnr else None, r.gpu_launches, r.compute)
 
 
 @dataclasses.dataclass
@@ -349,14 +373,19 @@ class Plan:
         _check(lib.tqsb_plan_stats(self._h, C.byref(n), C.byref(b)))
         return dict(classes=n.value, device_bytes=b.value)
 
+    def _call(self, config):
+        """The per-call configuration (None = the plan's own): like the reference's
+        shared KernelCache, the plan pins only the window and the tables."""
+        return None if config is None else C.byref(config._c())
+
     def reconstruct(self, frame: np.ndarray, reference: np.ndarray | None = None,
-                    out: np.ndarray | None = None) -> ReconstructionReport:
+                    out: np.ndarray | None = None,
+                    config: ReconstructionConfig | None = None) -> ReconstructionReport:
         frame = np.ascontiguousarray(frame, np.float64)
         if frame.ndim != 2:
             raise ValueError("frame must be 2-D")
         rows, cols = frame.shape
-        if out is None:
-            out = np.empty((2 * rows, 2 * cols))
+        out = _out_array(out, (2 * rows, 2 * cols))
         refp = None
         if reference is not None:
             reference = np.ascontiguousarray(reference, np.float64)
@@ -364,10 +393,12 @@ class Plan:
                 raise ValueError("reference dimensions do not match the reconstruction")
             refp = _d(reference)
         r = _Report()
-        _check(lib.tqsb_reconstruct(self._h, _d(frame), rows, cols, _d(out), refp, C.byref(r)))
+        _check(lib.tqsb_reconstruct_with(self._h, self._call(config), _d(frame), rows, cols,
+                                         _d(out), refp, C.byref(r)))
         return _report(out, r)
 
-    def reconstruct_batch(self, frames: list, outs: list | None = None) -> ReconstructionReport:
+    def reconstruct_batch(self, frames: list, outs: list | None = None,
+                          config: ReconstructionConfig | None = None) -> ReconstructionReport:
         """Frames of one shape through the pipelined multi-frame path (video stream)."""
         frames = [np.ascontiguousarray(f, np.float64) for f in frames]
         if not frames:
@@ -377,23 +408,27 @@ class Plan:
             raise ValueError("frames of a batch must share one shape")
         if outs is None:
             outs = [np.empty((2 * rows, 2 * cols)) for _ in frames]
+        if len(outs) != len(frames):
+            raise ValueError("outs must hold one output per frame")
+        outs = [_out_array(o, (2 * rows, 2 * cols), "outs[i]") for o in outs]
         fp = (_dp * len(frames))(*[_d(f) for f in frames])
         op = (_dp * len(outs))(*[_d(o) for o in outs])
         r = _Report()
-        _check(lib.tqsb_reconstruct_batch(self._h, fp, len(frames), rows, cols, op, C.byref(r)))
+        _check(lib.tqsb_reconstruct_batch_with(self._h, self._call(config), fp, len(frames), rows,
+                                               cols, op, C.byref(r)))
         return _report(outs, r)
 
     def reconstruct_band(self, frame: np.ndarray, br0: int, br1: int,
-                         out: np.ndarray | None = None) -> ReconstructionReport:
+                         out: np.ndarray | None = None,
+                         config: ReconstructionConfig | None = None) -> ReconstructionReport:
         frame = np.ascontiguousarray(frame, np.float64)
         rows, cols = frame.shape
-        B = self.config.block
+        B = (config or self.config).block
         r1 = min(br1 * B, 2 * rows)
-        if out is None:
-            out = np.empty((max(0, r1 - br0 * B), 2 * cols))
+        out = _out_array(out, (max(0, r1 - br0 * B), 2 * cols))
         r = _Report()
-        _check(lib.tqsb_reconstruct_band(self._h, _d(frame), rows, cols, br0, br1, _d(out),
-                                         C.byref(r)))
+        _check(lib.tqsb_reconstruct_band_with(self._h, self._call(config), _d(frame), rows, cols,
+                                              br0, br1, _d(out), C.byref(r)))
         return _report(out, r)
 
     def reconstruct_device(self, d_frame_ptr: int, rows: int, cols: int, d_out_ptr: int,
@@ -465,10 +500,10 @@ def reconstruct(frame: np.ndarray, pattern: QuadrantPattern, config: Reconstruct
     frame = np.ascontiguousarray(frame, np.float64)
     if frame.ndim != 2 or frame.size == 0:
         raise ValueError("empty measurement frame")
-    if cache is not None:
-        if cache.config.window != config.window:
-            raise LogicError("kernel cache holds a different window size")
-        return cache.reconstruct(frame, reference)
+    # the reference shares its cache with RL-JSDE only (pipeline.cpp:111-112): an
+    # L-JSDE call leaves the cache untouched and reports no cache counters
+    if cache is not None and config.algorithm == ALGO_RLJSDE:
+        return cache.reconstruct(frame, reference, config=config)
     with Plan(pattern, config, devices) as plan:
         return plan.reconstruct(frame, reference)
 

@@ -504,19 +504,6 @@ int run_compare(const std::string& pa, const std::string& pb, const std::string&
     return pass ? kExitOk : kExitCompareFailed;
 }
 
-// edge replication to even block multiples (pad_to_block_multiple, pipeline.cpp:187-209)
-tqsb::Image pad_to_block_multiple(const tqsb::Image& img, int block) {
-    if (block < 1) throw std::invalid_argument("block size must be positive");
-    if (img.rows < 1 || img.cols < 1) throw std::invalid_argument("empty image");
-    const int step = std::lcm(block, 2);
-    const int rows = (img.rows + step - 1) / step * step, cols = (img.cols + step - 1) / step * step;
-    if (rows == img.rows && cols == img.cols) return img;
-    tqsb::Image out(rows, cols);
-    for (int r = 0; r < rows; ++r)
-        for (int c = 0; c < cols; ++c) out.at(r, c) = img.at(std::min(r, img.rows - 1), std::min(c, img.cols - 1));
-    return out;
-}
-
 // bench (pipeline.cpp:258-329 / tqs.cpp:219-285) on the device: L-JSDE (fp64) and
 // RL-JSDE in its fp64 parity mode, both unclipped, must agree within the threshold;
 // (ext) the RL-JSDE fp32 product path is timed alongside.
@@ -547,7 +534,7 @@ int run_bench(const std::string& dir, const ReconstructArgs& a, bool scaling, do
     double sumL = 0, sumR = 0, sumWarm = 0, sumF = 0, maxDiff = 0;
     for (const tqsb::Image& img : images) {
         const tqsb::MeasurementFrame frame =
-            tqsb::simulate_measurement(pad_to_block_multiple(img, cfgL.block), pattern);
+            tqsb::simulate_measurement(tqsb::pad_to_block_multiple(img, cfgL.block).image, pattern);
         const tqsb::ReconstructionReport rl = tqsb::reconstruct(frame, pattern, cfgL);
         const tqsb::ReconstructionReport rr = tqsb::reconstruct(frame, pattern, cfgR, &cacheR);
         const tqsb::ReconstructionReport rf = tqsb::reconstruct(frame, pattern, cfgF, &cacheF);
@@ -570,7 +557,7 @@ int run_bench(const std::string& dir, const ReconstructArgs& a, bool scaling, do
     double lSmall = 0, lLarge = 0, rSmall = 0, rLarge = 0;
     if (scaling) {
         const tqsb::MeasurementFrame frame =
-            tqsb::simulate_measurement(pad_to_block_multiple(images.front(), cfgL.block), pattern);
+            tqsb::simulate_measurement(tqsb::pad_to_block_multiple(images.front(), cfgL.block).image, pattern);
         auto perBlock = [&](tqsb::Algorithm algo, int window) {
             tqsb::ReconstructionConfig c = algo == tqsb::Algorithm::Ljsde ? cfgL : cfgR;
             c.window = window;

@@ -85,17 +85,12 @@ int validate(const tqsb_config& c, int period) {
     return TQSB_OK;
 }
 
-// device-path limits (not in the reference): the fp32 product kernel holds a window
-// row/column per warp (W <= 32); larger windows run on the generic fp64 kernel
-int validate_device_limits(const tqsb_config& c) {
-    if (c.compute == TQSB_COMPUTE_FP32 && c.window <= kMaxWindowF32 && c.block * c.block > 256)
-        return set_error(TQSB_EINVAL, "block sizes above 16 require compute=fp64");
-    return TQSB_OK;
-}
-
-// the fp32 product kernel serves the plan (else the fp64 kernel: compute=fp64, or W > 32)
+// the fp32 product kernel serves the call (else the fp64 kernel: compute=fp64, or a
+// configuration outside the fp32 kernel's instantiations -- W > 32, where it holds a
+// window row per warp, or B > 16, beyond its 8 kept pixels per lane -- which the
+// reference accepts and the fp64 kernel runs on the reference's exact greedy paths)
 bool uses_f32(const tqsb_config& c) {
-    return c.compute == TQSB_COMPUTE_FP32 && c.window <= kMaxWindowF32;
+    return c.compute == TQSB_COMPUTE_FP32 && c.window <= kMaxWindowF32 && c.block * c.block <= 256;
 }
 
 // the fp64 RL-JSDE kernel on Precision::Single planes, like the reference's float
@@ -203,9 +198,22 @@ struct WindowTables {
     int W = 0, K = 0, NS = 0, K_pad = 0;
     std::vector<double> unit64;  // 2W
     std::vector<float> unit32;   // 2W
-    std::vector<double> q;       // K
     std::vector<int> perm, src;  // K_pad
 };
+
+// frequency_weights (basis.cpp:90-106): q_k = (1 - |centred k| / (sqrt2 (W/2)(1+1e-6)))^p
+std::vector<double> frequency_weights(int W, double exponent) {
+    std::vector<double> q(size_t(W) * W);
+    const int half = W / 2;
+    for (int s = 0; s < W; ++s)
+        for (int r = 0; r < W; ++r) {
+            const int cs = s <= half ? s : W - s, cr = r <= half ? r : W - r;
+            const double radius = std::sqrt(double(cs) * cs + double(cr) * cr);
+            const double maxr = 1.41421356237309504880 * half * (1.0 + 1e-6);
+            q[size_t(s) * W + r] = std::pow(1.0 - radius / maxr, exponent);
+        }
+    return q;
+}
 
 WindowTables window_tables(const tqsb_config& c) {
     WindowTables t;
@@ -229,7 +237,6 @@ WindowTables window_tables(const tqsb_config& c) {
     }
     t.unit32.resize(2 * W);
     for (int i = 0; i < 2 * W; ++i) t.unit32[i] = float(t.unit64[i]);
-    t.q.resize(t.K);
     const int half = W / 2;
     // Rank order: by centred radius (hot first), conjugate pairs k / -k on adjacent
     // ranks 2j (smaller flat k) and 2j+1, i.e. the two halves of one lane's slot, so
@@ -239,11 +246,8 @@ WindowTables window_tables(const tqsb_config& c) {
     // with (W/2, 0) at their radius.
     std::vector<std::tuple<int, int, int>> order;  // (group radius^2, pair id, k)
     for (int s = 0; s < W; ++s)
-        for (int r = 0; r < W; ++r) {  // frequency_weight (basis.cpp:90-97)
+        for (int r = 0; r < W; ++r) {
             const int cs = s <= half ? s : W - s, cr = r <= half ? r : W - r;
-            const double radius = std::sqrt(double(cs) * cs + double(cr) * cr);
-            const double maxr = 1.41421356237309504880 * half * (1.0 + 1e-6);
-            t.q[s * W + r] = std::pow(1.0 - radius / maxr, c.frequency_exponent);
             const int k = s * W + r, kc = ((W - s) % W) * W + (W - r) % W;
             int grp = cs * cs + cr * cr, pid = std::min(k, kc);
             if (k == kc && cs == half && cr == half) grp = 0, pid = 0;  // (W/2, W/2) next to DC
@@ -275,9 +279,10 @@ struct ClassSlab {
 };
 
 struct WorkKey {
-    int rows, cols, br0, br1;
+    int rows, cols, br0, br1, block, chunk;
     bool operator<(const WorkKey& o) const {
-        return std::tie(rows, cols, br0, br1) < std::tie(o.rows, o.cols, o.br0, o.br1);
+        return std::tie(rows, cols, br0, br1, block, chunk) <
+               std::tie(o.rows, o.cols, o.br0, o.br1, o.block, o.chunk);
     }
 };
 
@@ -291,10 +296,29 @@ struct Work {
     long long classes_total = 0, classes_interior = 0;
 };
 
+// The per-call derived tables of one option set. The cache proper is the fp64 planes
+// (B, C, D per offset class: the reference's KernelSet, rljsde.hpp:34-52), which
+// depend only on the pattern, the window and the spatial weights. The frequency
+// weights q (frequency exponent) and, for the fp32 product kernel, the scaled tables
+// s = sqrt(q/D), C' = s C and fac = gamma/(s D) depend on per-call options
+// (pipeline.cpp:108, 143-155), so they are derived from the planes lazily per
+// (exponent, gamma) -- k_scale + k_pack32, ~8 us per class -- and kept for reuse.
+struct Derived {
+    double exponent = 0.0, step = 0.0;  // step is 0 for fp64 sets (gamma is a kernel argument)
+    bool f32 = false;
+    double* d_q64 = nullptr;           // K frequency weights
+    std::vector<ClassSlab> slabs;      // per class slot: cpack, scale, fac (fp32 sets)
+    std::vector<ClassTab> tabs;        // per class slot: the planes + this set's tables
+    ClassTab* d_tabs = nullptr;
+    size_t d_tabs_cap = 0;
+    uint64_t last_use = 0;
+};
+constexpr size_t kMaxDerived = 4;     // option sets kept per device (LRU beyond)
+constexpr int kCounterRing = 64;      // per-launch task-queue heads (see launch())
+
 struct Device {
     int id = 0;
     int num_sms = 0;
-    int hot = 0;
     cudaStream_t stream = nullptr;            // solve
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // copy engines
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -303,14 +327,14 @@ struct Device {
     int* d_src = nullptr;
     float* d_unit32 = nullptr;
     double* d_unit64 = nullptr;
-    double* d_q64 = nullptr;
     uint8_t* d_opaque = nullptr;   // the pattern's (P/2)^2 quadrant indices (device readout)
-    int* d_counter = nullptr;      // dynamic task queue head of the fp32 solve
+    int* d_counters = nullptr;     // kCounterRing dynamic task-queue heads
+    unsigned counter_next = 0;
     std::map<int, int> slot_of;    // class key -> slot
-    std::vector<ClassTab> tabs;    // host mirror
+    std::vector<ClassTab> tabs;    // host mirror of the planes per slot (derived fields null)
     std::vector<ClassSlab> slabs;
-    ClassTab* d_tabs = nullptr;
-    size_t d_tabs_cap = 0;
+    std::vector<std::unique_ptr<Derived>> derived;
+    uint64_t use_clock = 0;
     std::map<WorkKey, Work> works;
     double* d_frame = nullptr;
     size_t frame_cap = 0;
@@ -360,41 +384,38 @@ int device_init(tqsb_plan* p, Device* d) {
     CUDA_TRY(cudaMalloc(&d->d_src, sizeof(int) * t.K_pad));
     CUDA_TRY(cudaMalloc(&d->d_unit32, sizeof(float) * 2 * t.W));
     CUDA_TRY(cudaMalloc(&d->d_unit64, sizeof(double) * 2 * t.W));
-    CUDA_TRY(cudaMalloc(&d->d_q64, sizeof(double) * t.K));
     CUDA_TRY(cudaMalloc(&d->d_opaque, p->opaque.size()));
-    CUDA_TRY(cudaMalloc(&d->d_counter, sizeof(int)));
+    CUDA_TRY(cudaMalloc(&d->d_counters, sizeof(int) * kCounterRing));
     CUDA_TRY(cudaMemcpy(d->d_opaque, p->opaque.data(), p->opaque.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_perm, t.perm.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_src, t.src.data(), sizeof(int) * t.K_pad, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_unit32, t.unit32.data(), sizeof(float) * 2 * t.W, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d->d_unit64, t.unit64.data(), sizeof(double) * 2 * t.W, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d->d_q64, t.q.data(), sizeof(double) * t.K, cudaMemcpyHostToDevice));
-    const int maxhot = solve_f32_max_hot(t.NS, d->id);
-    const int K_pad = t.K_pad;
-    // auto (-1): no TMEM tier -- with predicated per-chunk loads it costs more issue slots
-    // than it saves (4K frame: 40.6 ms with 8 hot columns vs 40.1 ms without)
-    int hot = p->cfg.hot_columns < 0 ? 0 : std::min(p->cfg.hot_columns, maxhot);
-    d->hot = std::clamp(hot, 0, K_pad);
     return TQSB_OK;
+}
+
+void derived_free(Derived* v) {
+    for (auto& s : v->slabs) cudaFree(s.base);
+    cudaFree(v->d_tabs);
+    cudaFree(v->d_q64);
 }
 
 void device_free(Device* d) {
     if (!d) return;
     cudaSetDevice(d->id);
     for (auto& s : d->slabs) cudaFree(s.base);
+    for (auto& v : d->derived) derived_free(v.get());
     for (auto& kv : d->works) {
         cudaFree(kv.second.d_tasks);
         cudaFree(kv.second.d_items);
         cudaFree(kv.second.d_task_cls);
     }
-    cudaFree(d->d_tabs);
     cudaFree(d->d_perm);
     cudaFree(d->d_src);
     cudaFree(d->d_unit32);
     cudaFree(d->d_unit64);
-    cudaFree(d->d_q64);
     cudaFree(d->d_opaque);
-    cudaFree(d->d_counter);
+    cudaFree(d->d_counters);
     cudaFree(d->d_frame);
     cudaFree(d->d_out);
     if (d->h_in) cudaFreeHost(d->h_in);
@@ -439,14 +460,15 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     for (auto& t : th) t.join();
 }
 
-// Allocate the device slab of one class (fp64 planes, fp32 product tables, local
-// system) on device d, upload its local system and register it under `key`;
-// cb receives the build descriptor.
-int alloc_class(tqsb_plan* p, Device* d, int key, int orow, int ocol, ClassBuild* cb) {
+// Allocate the device slab of one class's fp64 planes (and its local system) on
+// device d, upload the local system and register it under `key`; cb receives the
+// build descriptor. The spatial weights come from the config of the call that
+// creates the class, like the reference's make_kernels (pipeline.cpp:114-121).
+int alloc_class(tqsb_plan* p, Device* d, const tqsb_config& c, int key, int orow, int ocol,
+                ClassBuild* cb) {
     const WindowTables& t = p->wt;
-    const size_t K = t.K, K_pad = t.K_pad, W = t.W;
-    const bool f32 = uses_f32(p->cfg);  // fp32 product tables only for the fp32 kernel
-    LocalSystem ls = local_system(p->opaque, p->period, orow, ocol, p->cfg);
+    const size_t K = t.K, W = t.W;
+    LocalSystem ls = local_system(p->opaque, p->period, orow, ocol, c);
     const size_t L = ls.L;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -455,10 +477,8 @@ int alloc_class(tqsb_plan* p, Device* d, int key, int orow, int ocol, ClassBuild
         return o;
     };
     const size_t o_c64 = take(K * K * 2 * 8), o_b64 = take(K * L * 2 * 8),
-                 o_t64 = take(K * L * 2 * 8), o_d64 = take(K * 8),
-                 o_cpack = f32 ? take(K_pad * K_pad * 8) : 0, o_scale = f32 ? take(K_pad * 4) : 0,
-                 o_fac = f32 ? take(K_pad * 4) : 0, o_mask = take(W * W * 4), o_px = take(L * 12 + 8),
-                 o_w = take(L * 8 + 8);
+                 o_t64 = take(K * L * 2 * 8), o_d64 = take(K * 8), o_mask = take(W * W * 4),
+                 o_px = take(L * 12 + 8), o_w = take(L * 8 + 8);
     ClassSlab slab;
     slab.bytes = off;
     CUDA_TRY(cudaMalloc(&slab.base, slab.bytes));
@@ -476,13 +496,7 @@ int alloc_class(tqsb_plan* p, Device* d, int key, int orow, int ocol, ClassBuild
     cb->b64 = reinterpret_cast<double*>(b + o_b64);
     cb->c64 = reinterpret_cast<double*>(b + o_c64);
     cb->d64 = reinterpret_cast<double*>(b + o_d64);
-    cb->cpack = f32 ? reinterpret_cast<float*>(b + o_cpack) : nullptr;
-    cb->scale = f32 ? reinterpret_cast<float*>(b + o_scale) : nullptr;
-    cb->fac = f32 ? reinterpret_cast<float*>(b + o_fac) : nullptr;
     ClassTab tab{};
-    tab.cpack = cb->cpack;
-    tab.scale = cb->scale;
-    tab.fac = cb->fac;
     tab.mask32 = reinterpret_cast<const float*>(b + o_mask);
     tab.b64 = cb->b64;
     tab.c64 = cb->c64;
@@ -497,24 +511,10 @@ int alloc_class(tqsb_plan* p, Device* d, int key, int orow, int ocol, ClassBuild
     return TQSB_OK;
 }
 
-// refresh the device ClassTab array after classes were added
-int publish_tabs(Device* d) {
-    if (d->tabs.size() > d->d_tabs_cap) {
-        CUDA_TRY(cudaStreamSynchronize(d->stream));
-        cudaFree(d->d_tabs);
-        d->d_tabs_cap = std::max<size_t>(d->tabs.size() * 2, 16);
-        CUDA_TRY(cudaMalloc(&d->d_tabs, sizeof(ClassTab) * d->d_tabs_cap));
-    }
-    CUDA_TRY(cudaMemcpyAsync(d->d_tabs, d->tabs.data(), sizeof(ClassTab) * d->tabs.size(),
-                             cudaMemcpyHostToDevice, d->stream));
-    CUDA_TRY(cudaStreamSynchronize(d->stream));
-    return TQSB_OK;
-}
-
-// Build the tables of every class in `keys` that is not resident on device d
+// Build the fp64 planes of every class in `keys` that is not resident on device d
 // (batched; the serial warm pass of pipeline.cpp:127-133). Returns the number of
 // classes created through *created.
-int ensure_classes(tqsb_plan* p, Device* d, const std::vector<int>& keys,
+int ensure_classes(tqsb_plan* p, Device* d, const tqsb_config& c, const std::vector<int>& keys,
                    const std::map<int, std::pair<int, int>>& rep, int* created, int* launches) {
     std::vector<int> missing;
     for (int k : keys)
@@ -527,32 +527,124 @@ int ensure_classes(tqsb_plan* p, Device* d, const std::vector<int>& keys,
     for (int key : missing) {
         const auto [orow, ocol] = rep.at(key);
         ClassBuild cb;
-        TQSB_TRY(alloc_class(p, d, key, orow, ocol, &cb));
+        TQSB_TRY(alloc_class(p, d, c, key, orow, ocol, &cb));
         max_local = std::max(max_local, cb.local);
         descs.push_back(cb);
     }
-    int rc = launch_tables_batch(descs.data(), int(descs.size()), p->wt.W, p->wt.K_pad,
-                                 p->cfg.step_width, d->d_unit64, d->d_q64, d->d_perm, max_local,
-                                 d->stream, launches, 0, round_single(p->cfg));
+    int rc = launch_tables_build(descs.data(), int(descs.size()), p->wt.W, d->d_unit64, max_local,
+                                 d->stream, launches, round_single(c));
     if (rc != 0) return set_error(TQSB_ECUDA, std::string("table build: ") +
                                                   cudaGetErrorString(cudaError_t(rc)));
-    return publish_tabs(d);
+    CUDA_TRY(cudaStreamSynchronize(d->stream));
+    return TQSB_OK;
+}
+
+// The derived tables of the call's options on device d, extended to every resident
+// class (see Derived). Least recently used sets beyond kMaxDerived are released.
+int ensure_derived(tqsb_plan* p, Device* d, const tqsb_config& c, Derived** out, int* launches) {
+    const bool f32 = uses_f32(c);
+    const double step = f32 ? c.step_width : 0.0;
+    Derived* dv = nullptr;
+    for (auto& x : d->derived)
+        if (x->f32 == f32 && x->exponent == c.frequency_exponent && x->step == step) dv = x.get();
+    CUDA_TRY(cudaSetDevice(d->id));
+    const WindowTables& t = p->wt;
+    if (!dv) {
+        if (d->derived.size() >= kMaxDerived) {
+            auto lru = std::min_element(d->derived.begin(), d->derived.end(),
+                                        [](const auto& x, const auto& y) { return x->last_use < y->last_use; });
+            CUDA_TRY(cudaDeviceSynchronize());  // device-API launches may still read it
+            for (auto& sl : (*lru)->slabs) d->table_bytes -= sl.bytes;
+            derived_free(lru->get());
+            d->derived.erase(lru);
+        }
+        auto nd = std::make_unique<Derived>();
+        nd->exponent = c.frequency_exponent;
+        nd->step = step;
+        nd->f32 = f32;
+        const std::vector<double> q = frequency_weights(t.W, c.frequency_exponent);
+        CUDA_TRY(cudaMalloc(&nd->d_q64, sizeof(double) * t.K));
+        CUDA_TRY(cudaMemcpy(nd->d_q64, q.data(), sizeof(double) * t.K, cudaMemcpyHostToDevice));
+        dv = nd.get();
+        d->derived.push_back(std::move(nd));
+    }
+    dv->last_use = ++d->use_clock;
+    const size_t n0 = dv->tabs.size(), n = d->tabs.size();
+    if (n0 < n) {
+        const size_t K_pad = t.K_pad;
+        std::vector<ClassBuild> descs;
+        for (size_t i = n0; i < n; ++i) {
+            ClassTab tab = d->tabs[i];
+            ClassSlab slab;
+            if (f32) {
+                const size_t o_cpack = 0, o_scale = align_up(K_pad * K_pad * 8, 256),
+                             o_fac = o_scale + align_up(K_pad * 4, 256);
+                slab.bytes = o_fac + align_up(K_pad * 4, 256);
+                CUDA_TRY(cudaMalloc(&slab.base, slab.bytes));
+                char* b = static_cast<char*>(slab.base);
+                ClassBuild cb{};
+                cb.local = tab.local;
+                cb.c64 = const_cast<double*>(tab.c64);
+                cb.d64 = const_cast<double*>(tab.d64);
+                cb.cpack = reinterpret_cast<float*>(b + o_cpack);
+                cb.scale = reinterpret_cast<float*>(b + o_scale);
+                cb.fac = reinterpret_cast<float*>(b + o_fac);
+                tab.cpack = cb.cpack;
+                tab.scale = cb.scale;
+                tab.fac = cb.fac;
+                descs.push_back(cb);
+                d->table_bytes += slab.bytes;
+            }
+            dv->slabs.push_back(slab);
+            dv->tabs.push_back(tab);
+        }
+        if (!descs.empty()) {
+            const int rc = launch_tables_derive(descs.data(), int(descs.size()), t.W, t.K_pad, step,
+                                                dv->d_q64, d->d_perm, d->stream, launches);
+            if (rc != 0)
+                return set_error(TQSB_ECUDA, std::string("table derive: ") +
+                                                 cudaGetErrorString(cudaError_t(rc)));
+        }
+        if (dv->tabs.size() > dv->d_tabs_cap) {
+            CUDA_TRY(cudaStreamSynchronize(d->stream));
+            cudaFree(dv->d_tabs);
+            dv->d_tabs = nullptr;
+            dv->d_tabs_cap = std::max<size_t>(dv->tabs.size() * 2, 16);
+            CUDA_TRY(cudaMalloc(&dv->d_tabs, sizeof(ClassTab) * dv->d_tabs_cap));
+        }
+        CUDA_TRY(cudaMemcpyAsync(dv->d_tabs, dv->tabs.data(), sizeof(ClassTab) * dv->tabs.size(),
+                                 cudaMemcpyHostToDevice, d->stream));
+        CUDA_TRY(cudaStreamSynchronize(d->stream));
+    }
+    *out = dv;
+    return TQSB_OK;
 }
 
 // Class-sorted tasks and CTA work items for a band of block rows on device d;
 // the band's classes are made resident first (cached per frame shape and band).
-int prepare_band(tqsb_plan* p, Device* d, const Geometry& g, int frame_rows, int frame_cols,
-                 int br0, int br1, Work** out, int* created, int* launches) {
+int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& g, int frame_rows,
+                 int frame_cols, int br0, int br1, Work** out, int* created, int* launches) {
     *created = 0;
-    const WorkKey wkey{frame_rows, frame_cols, br0, br1};
+    const int chunk = (uses_f32(c) ? kWarpsF32 : kWarpsF64) * 4;
+    const WorkKey wkey{frame_rows, frame_cols, br0, br1, g.B, chunk};
+    Enumerated e;
     auto it = d->works.find(wkey);
+    if (it != d->works.end()) {
+        // the work list is cached; its classes may have been created under another
+        // option set, so make sure they are (still) resident
+        bool all = true;
+        for (int k : it->second.keys) all = all && d->slot_of.count(k);
+        if (all) {
+            *out = &it->second;
+            return TQSB_OK;
+        }
+    }
+    enumerate(g, p->period, br0, br1, &e);
+    TQSB_TRY(ensure_classes(p, d, c, e.class_order, e.representative, created, launches));
     if (it != d->works.end()) {
         *out = &it->second;
         return TQSB_OK;
     }
-    Enumerated e;
-    enumerate(g, p->period, br0, br1, &e);
-    TQSB_TRY(ensure_classes(p, d, e.class_order, e.representative, created, launches));
     Work w;
     w.keys = e.class_order;
     w.classes_total = e.classes_total;
@@ -574,7 +666,6 @@ int prepare_band(tqsb_plan* p, Device* d, const Geometry& g, int frame_rows, int
     std::vector<int> task_cls;
     sorted.reserve(e.tasks.size());
     task_cls.reserve(e.tasks.size());
-    const int chunk = (p->cfg.compute == TQSB_COMPUTE_FP32 ? kWarpsF32 : kWarpsF64) * 4;
     for (int k : e.class_order) {
         const auto& v = by_key[k];
         for (size_t s = 0; s < v.size(); s += chunk) {
@@ -588,7 +679,6 @@ int prepare_band(tqsb_plan* p, Device* d, const Geometry& g, int frame_rows, int
         task_cls.insert(task_cls.end(), v.size(), d->slot_of.at(k));
     }
     w.n_items = int(items.size());
-    (void)frame_cols;
     CUDA_TRY(cudaSetDevice(d->id));
     CUDA_TRY(cudaMalloc(&w.d_tasks, sizeof(Task) * std::max<size_t>(1, sorted.size())));
     CUDA_TRY(cudaMalloc(&w.d_items, sizeof(WorkItem) * std::max<size_t>(1, items.size())));
@@ -634,33 +724,40 @@ bool is_pinned(const void* p) {
     return at.type == cudaMemoryTypeHost;
 }
 
-SolveArgs base_args(tqsb_plan* p, Device* d) {
+// kernel arguments of one call: the call's solver options (nu, gamma, clip, block,
+// early stop) over the derived tables of its option set
+SolveArgs base_args(tqsb_plan* p, Device* d, const tqsb_config& c, const Derived* dv) {
     SolveArgs a{};
-    a.tabs = d->d_tabs;
+    a.tabs = dv->d_tabs;
     a.wc.perm = d->d_perm;
     a.wc.src = d->d_src;
     a.wc.unit32 = d->d_unit32;
     a.wc.unit64 = d->d_unit64;
-    a.wc.q64 = d->d_q64;
-    a.window = p->cfg.window;
-    a.block = p->cfg.block;
-    a.iterations = p->cfg.max_iterations;
-    a.step = p->cfg.step_width;
-    a.clip = p->cfg.clip_output;
-    a.hot = d->hot;
-    a.early_stop = p->cfg.early_stop;
-    a.early_stop_scale = p->cfg.early_stop_scale;
-    a.counter = d->d_counter;
+    a.wc.q64 = dv->d_q64;
+    a.window = c.window;
+    a.block = c.block;
+    a.iterations = c.max_iterations;
+    a.step = c.step_width;
+    a.clip = c.clip_output;
+    // TMEM column tier: off unless asked for (auto = 0; with predicated per-chunk loads it
+    // costs more issue slots than it saves: 4K frame 40.6 ms with 8 hot columns vs 40.1)
+    const int maxhot = std::min(solve_f32_max_hot(p->wt.NS, d->id), p->wt.K_pad);
+    a.hot = uses_f32(c) && c.hot_columns > 0 ? std::min(c.hot_columns, maxhot) : 0;
+    a.early_stop = c.early_stop;
+    a.early_stop_scale = c.early_stop_scale;
+    // a fresh queue head per launch (zeroed on the launch stream in launch()), so
+    // reconstructions in flight on different streams never share one
+    a.counter = d->d_counters + (d->counter_next++ % kCounterRing);
     return a;
 }
 
-int launch(tqsb_plan* p, Device* d, const SolveArgs& a, cudaStream_t s) {
+int launch(const tqsb_config& c, Device* d, const SolveArgs& a, cudaStream_t s, int n_slots) {
     if (a.counter) CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
     int rc;
-    if (p->cfg.algorithm == TQSB_ALGO_LJSDE) {
+    if (c.algorithm == TQSB_ALGO_LJSDE) {
         rc = launch_solve_ljsde(a, s, d->num_sms);
-    } else if (uses_f32(p->cfg)) {
-        rc = launch_solve_f32(a, p->wt.NS, s, d->num_sms);
+    } else if (uses_f32(c)) {
+        rc = launch_solve_f32(a, n_slots, s, d->num_sms);
     } else {  // fp64 mode: register-resident kernel where it applies, else the general one
         rc = launch_solve_f64r(a, s, d->num_sms);
         if (rc == cudaErrorNotSupported) rc = launch_solve_f64(a, s, d->num_sms);
@@ -681,23 +778,23 @@ struct BandResult {
     long long classes_total = 0, classes_interior = 0, blocks = 0;
 };
 
-// Host-buffer band run on device d: H2D of the band's frame rows (pinned
-// staging), solve, D2H of the band's output rows.
 // Host-buffer band run on device d: H2D of the band's frame rows (halo included),
 // one solve launch whose B x B output tiles are stored straight into pinned host
 // memory (zero-copy: the caller's buffer when it is pinned, else the plan's pinned
 // staging), so the output transfer overlaps the solve instead of following it.
-void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* frame,
-                   int frame_rows, int frame_cols, int br0, int br1, double* out_band,
-                   BandResult* r) {
+void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& g,
+                   const double* frame, int frame_rows, int frame_cols, int br0, int br1,
+                   double* out_band, BandResult* r) {
     auto fail = [&](int rc) {
         r->rc = rc;
         r->err = g_error;
     };
     if (cudaSetDevice(d->id) != cudaSuccess) return fail(set_error(TQSB_ECUDA, "cudaSetDevice"));
     Work* w = nullptr;
+    Derived* dv = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    int rc = prepare_band(p, d, g, frame_rows, frame_cols, br0, br1, &w, &r->created, &r->launches);
+    int rc = prepare_band(p, d, c, g, frame_rows, frame_cols, br0, br1, &w, &r->created, &r->launches);
+    if (!rc) rc = ensure_derived(p, d, c, &dv, &r->launches);
     if (rc) return fail(rc);
     r->warm = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     r->classes_total = w->classes_total;
@@ -723,7 +820,7 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
         return fail(set_error(TQSB_ECUDA, "output buffer is not device-mapped pinned memory"));
     }
     cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
-    SolveArgs a = base_args(p, d);
+    SolveArgs a = base_args(p, d, c, dv);
     a.frame = d->d_frame;
     a.frame_rows = frame_rows;
     a.frame_cols = frame_cols;
@@ -740,7 +837,7 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
     a.n_tasks = w->n_tasks;
     cudaEventRecord(d->ev0, d->stream);
     if (w->n_items > 0) {
-        if ((rc = launch(p, d, a, d->stream))) return fail(rc);
+        if ((rc = launch(c, d, a, d->stream, p->wt.NS))) return fail(rc);
         r->launches += 1;
     }
     cudaEventRecord(d->ev1, d->stream);
@@ -754,8 +851,9 @@ void run_band_host(tqsb_plan* p, Device* d, const Geometry& g, const double* fra
 // Multi-frame pipeline on one device: frame i+1's H2D (copy stream) overlaps frame
 // i's solve; outputs are stored zero-copy into pinned host memory by the kernel.
 // Pageable frames/outputs go through double-buffered pinned staging.
-void run_batch_host(tqsb_plan* p, Device* d, const Geometry& g, const double* const* frames,
-                    int frame_rows, int frame_cols, double* const* outs, int n, BandResult* r) {
+void run_batch_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& g,
+                    const double* const* frames, int frame_rows, int frame_cols,
+                    double* const* outs, int n, BandResult* r) {
     auto fail = [&](int rc) {
         r->rc = rc;
         r->err = g_error;
@@ -763,9 +861,11 @@ void run_batch_host(tqsb_plan* p, Device* d, const Geometry& g, const double* co
     if (n <= 0) return;
     if (cudaSetDevice(d->id) != cudaSuccess) return fail(set_error(TQSB_ECUDA, "cudaSetDevice"));
     Work* w = nullptr;
+    Derived* dv = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     const int nbr = g.padM / g.B;
-    int rc = prepare_band(p, d, g, frame_rows, frame_cols, 0, nbr, &w, &r->created, &r->launches);
+    int rc = prepare_band(p, d, c, g, frame_rows, frame_cols, 0, nbr, &w, &r->created, &r->launches);
+    if (!rc) rc = ensure_derived(p, d, c, &dv, &r->launches);
     if (rc) return fail(rc);
     r->warm = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     r->classes_total = w->classes_total;
@@ -792,20 +892,19 @@ void run_batch_host(tqsb_plan* p, Device* d, const Geometry& g, const double* co
         cudaMemcpyAsync(d->d_fs[s], src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->s_h2d);
         cudaEventRecord(d->ev_h2d[s], d->s_h2d);
         cudaStreamWaitEvent(d->stream, d->ev_h2d[s], 0);
-        double* host_out = outs[i];
-        if (!out_pinned[i]) {
-            if (i >= 2) {  // frame i-2's kernel wrote h_out_s[s]; hand it over first
-                cudaEventSynchronize(d->ev_comp[s]);
-                if (!out_pinned[i - 2]) par_memcpy(outs[i - 2], d->h_out_s[s], sizeof(double) * out_n);
-            }
-            host_out = d->h_out_s[s];
+        // frame i-2 staged its output in h_out_s[s]: hand it over before anything may
+        // reuse the slot (whether or not frame i needs staging itself)
+        if (i >= 2 && !out_pinned[i - 2]) {
+            cudaEventSynchronize(d->ev_comp[s]);
+            par_memcpy(outs[i - 2], d->h_out_s[s], sizeof(double) * out_n);
         }
+        double* host_out = out_pinned[i] ? outs[i] : d->h_out_s[s];
         double* dev_view = nullptr;
         if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_view), host_out, 0) != cudaSuccess) {
             cudaGetLastError();
             return fail(set_error(TQSB_ECUDA, "output buffer is not device-mapped pinned memory"));
         }
-        SolveArgs a = base_args(p, d);
+        SolveArgs a = base_args(p, d, c, dv);
         a.frame = d->d_fs[s];
         a.frame_rows = frame_rows;
         a.frame_cols = frame_cols;
@@ -822,7 +921,7 @@ void run_batch_host(tqsb_plan* p, Device* d, const Geometry& g, const double* co
         a.n_tasks = w->n_tasks;
         if (i == 0) cudaEventRecord(d->ev0, d->stream);
         if (w->n_items > 0) {
-            if ((rc = launch(p, d, a, d->stream))) return fail(rc);
+            if ((rc = launch(c, d, a, d->stream, p->wt.NS))) return fail(rc);
             r->launches += 1;
         }
         cudaEventRecord(d->ev_comp[s], d->stream);
@@ -836,7 +935,7 @@ void run_batch_host(tqsb_plan* p, Device* d, const Geometry& g, const double* co
     cudaEventElapsedTime(&r->ms, d->ev0, d->ev1);
 }
 
-void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const Geometry& g,
+void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const tqsb_config& c,
                  long long classes_total, long long classes_interior, double e2e) {
     if (!rep) return;
     std::memset(rep, 0, sizeof(*rep));
@@ -863,13 +962,13 @@ void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const Geom
     rep->psnr_db = 0.0;
     rep->has_psnr = 0;
     rep->gpu_launches = launches;
-    (void)g;
+    rep->compute = uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE ? TQSB_COMPUTE_FP32 : TQSB_COMPUTE_FP64;
 }
 
 // L-JSDE keeps no kernel cache in the reference (pipeline.cpp:111-112, 173-177):
 // its report carries no cache counters (the device still builds B and D per class)
-void ljsde_report(const tqsb_plan* p, tqsb_report* rep) {
-    if (!rep || p->cfg.algorithm != TQSB_ALGO_LJSDE) return;
+void ljsde_report(const tqsb_config& c, tqsb_report* rep) {
+    if (!rep || c.algorithm != TQSB_ALGO_LJSDE) return;
     rep->classes_created = 0;
     rep->cache_hits = 0;
     rep->cache_misses = 0;
@@ -945,7 +1044,6 @@ int tqsb_plan_create(const uint8_t* opaque, int period, const tqsb_config* cfg,
     if (period < 4 || period % 2 != 0)
         return set_error(TQSB_EINVAL, "pattern period must be even and >= 4");
     TQSB_TRY(validate(*cfg, period));
-    TQSB_TRY(validate_device_limits(*cfg));
     if (n_devices < 1) return set_error(TQSB_EINVAL, "at least one device is required");
     const int have = tqsb_device_count();
     if (have < 1) return set_error(TQSB_ENODEV, "no CUDA device available (no CPU fallback)");
@@ -996,7 +1094,10 @@ int tqsb_plan_warm(tqsb_plan* p, int frame_rows, int frame_cols, double* warm_se
     enumerate(g, p->period, 0, g.padM / g.B, &e);
     for (auto& d : p->devs) {
         int created = 0, launches = 0;
-        TQSB_TRY(ensure_classes(p, d.get(), e.class_order, e.representative, &created, &launches));
+        Derived* dv = nullptr;
+        TQSB_TRY(ensure_classes(p, d.get(), p->cfg, e.class_order, e.representative, &created,
+                                &launches));
+        TQSB_TRY(ensure_derived(p, d.get(), p->cfg, &dv, &launches));
     }
     for (auto& d : p->devs) {
         cudaSetDevice(d->id);
@@ -1007,44 +1108,69 @@ int tqsb_plan_warm(tqsb_plan* p, int frame_rows, int frame_cols, double* warm_se
     return TQSB_OK;
 }
 
-int tqsb_reconstruct_band(tqsb_plan* p, const double* frame, int frame_rows, int frame_cols,
-                          int br0, int br1, double* out_band, tqsb_report* rep) {
-    if (!p || !frame || !out_band) return set_error(TQSB_EINVAL, "null argument");
-    std::lock_guard<std::mutex> lk(p->mu);
-    const auto t0 = std::chrono::steady_clock::now();
-    Geometry g;
-    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
-    if (br0 < 0 || br1 > g.padM / g.B || br0 > br1)
-        return set_error(TQSB_EINVAL, "block-row band out of range");
-    std::vector<BandResult> rs(1);
-    run_band_host(p, p->devs[0].get(), g, frame, frame_rows, frame_cols, br0, br1, out_band, &rs[0]);
-    if (rs[0].rc) return set_error(rs[0].rc, rs[0].err);
-    fill_report(rep, rs, g, rs[0].classes_total, rs[0].classes_interior,
-                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
-    ljsde_report(p, rep);
+} // extern "C"
+
+namespace {
+
+// The configuration a call runs with: the plan's own, or the caller's per-call config
+// over the plan's tables (the reference's shared KernelCache: each call brings its own
+// q, nu, gamma, block, clip and algorithm, pipeline.cpp:108-166; the cache only pins
+// the window, pipeline.cpp:146-147).
+int call_config(const tqsb_plan* p, const tqsb_config* call, tqsb_config* out) {
+    if (!call) {
+        *out = p->cfg;
+        return TQSB_OK;
+    }
+    TQSB_TRY(validate(*call, p->period));
+    if (call->window != p->cfg.window)
+        return set_error(TQSB_ELOGIC, "kernel cache holds a different window size");
+    *out = *call;
     return TQSB_OK;
 }
 
-int tqsb_reconstruct(tqsb_plan* p, const double* frame, int frame_rows, int frame_cols,
-                     double* out, const double* reference, tqsb_report* rep) {
+int reconstruct_band_impl(tqsb_plan* p, const tqsb_config* call, const double* frame,
+                          int frame_rows, int frame_cols, int br0, int br1, double* out_band,
+                          tqsb_report* rep) {
+    if (!p || !frame || !out_band) return set_error(TQSB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    const auto t0 = std::chrono::steady_clock::now();
+    tqsb_config c;
+    TQSB_TRY(call_config(p, call, &c));
+    Geometry g;
+    TQSB_TRY(geometry(c, frame_rows, frame_cols, &g));
+    if (br0 < 0 || br1 > g.padM / g.B || br0 > br1)
+        return set_error(TQSB_EINVAL, "block-row band out of range");
+    std::vector<BandResult> rs(1);
+    run_band_host(p, p->devs[0].get(), c, g, frame, frame_rows, frame_cols, br0, br1, out_band, &rs[0]);
+    if (rs[0].rc) return set_error(rs[0].rc, rs[0].err);
+    fill_report(rep, rs, c, rs[0].classes_total, rs[0].classes_interior,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    ljsde_report(c, rep);
+    return TQSB_OK;
+}
+
+int reconstruct_impl(tqsb_plan* p, const tqsb_config* call, const double* frame, int frame_rows,
+                     int frame_cols, double* out, const double* reference, tqsb_report* rep) {
     if (!p || !frame || !out) return set_error(TQSB_EINVAL, "null argument");
     std::lock_guard<std::mutex> lk(p->mu);
     const auto t0 = std::chrono::steady_clock::now();
+    tqsb_config c;
+    TQSB_TRY(call_config(p, call, &c));
     Geometry g;
-    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    TQSB_TRY(geometry(c, frame_rows, frame_cols, &g));
     const int nbr = g.padM / g.B;
     const int nd = std::min<int>(int(p->devs.size()), std::max(1, nbr));
     std::vector<BandResult> rs(nd);
     std::vector<int> cut(nd + 1);
     for (int i = 0; i <= nd; ++i) cut[i] = int((long long)nbr * i / nd);
     if (nd == 1) {
-        run_band_host(p, p->devs[0].get(), g, frame, frame_rows, frame_cols, 0, nbr, out, &rs[0]);
+        run_band_host(p, p->devs[0].get(), c, g, frame, frame_rows, frame_cols, 0, nbr, out, &rs[0]);
     } else {
         std::vector<std::thread> th;
         for (int i = 0; i < nd; ++i)
             th.emplace_back([&, i] {
                 double* ob = out + size_t(cut[i]) * g.B * g.N;
-                run_band_host(p, p->devs[i].get(), g, frame, frame_rows, frame_cols, cut[i],
+                run_band_host(p, p->devs[i].get(), c, g, frame, frame_rows, frame_cols, cut[i],
                               cut[i + 1], ob, &rs[i]);
             });
         for (auto& t : th) t.join();
@@ -1060,8 +1186,8 @@ int tqsb_reconstruct(tqsb_plan* p, const double* frame, int frame_rows, int fram
         ci = e.classes_interior;
     }
     const double e2e = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    fill_report(rep, rs, g, ct, ci, e2e);
-    ljsde_report(p, rep);
+    fill_report(rep, rs, c, ct, ci, e2e);
+    ljsde_report(c, rep);
     if (reference) {
         const double v = psnr_impl(reference, out, (long long)g.M * g.N);
         if (rep) {
@@ -1072,26 +1198,29 @@ int tqsb_reconstruct(tqsb_plan* p, const double* frame, int frame_rows, int fram
     return TQSB_OK;
 }
 
-int tqsb_reconstruct_batch(tqsb_plan* p, const double* const* frames, int n_frames,
-                           int frame_rows, int frame_cols, double* const* outs, tqsb_report* rep) {
+int reconstruct_batch_impl(tqsb_plan* p, const tqsb_config* call, const double* const* frames,
+                           int n_frames, int frame_rows, int frame_cols, double* const* outs,
+                           tqsb_report* rep) {
     if (!p || !frames || !outs || n_frames < 0) return set_error(TQSB_EINVAL, "null argument");
     for (int i = 0; i < n_frames; ++i)
         if (!frames[i] || !outs[i]) return set_error(TQSB_EINVAL, "null frame or output pointer");
     std::lock_guard<std::mutex> lk(p->mu);
     const auto t0 = std::chrono::steady_clock::now();
+    tqsb_config c;
+    TQSB_TRY(call_config(p, call, &c));
     Geometry g;
-    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    TQSB_TRY(geometry(c, frame_rows, frame_cols, &g));
     const int nd = std::max(1, std::min<int>(int(p->devs.size()), n_frames));
     std::vector<BandResult> rs(nd);
     std::vector<int> cut(nd + 1);
     for (int i = 0; i <= nd; ++i) cut[i] = int((long long)n_frames * i / nd);
     if (nd == 1) {
-        run_batch_host(p, p->devs[0].get(), g, frames, frame_rows, frame_cols, outs, n_frames, &rs[0]);
+        run_batch_host(p, p->devs[0].get(), c, g, frames, frame_rows, frame_cols, outs, n_frames, &rs[0]);
     } else {  // whole frames per device, one host thread each
         std::vector<std::thread> th;
         for (int i = 0; i < nd; ++i)
             th.emplace_back([&, i] {
-                run_batch_host(p, p->devs[i].get(), g, frames + cut[i], frame_rows, frame_cols,
+                run_batch_host(p, p->devs[i].get(), c, g, frames + cut[i], frame_rows, frame_cols,
                                outs + cut[i], cut[i + 1] - cut[i], &rs[i]);
             });
         for (auto& t : th) t.join();
@@ -1099,24 +1228,28 @@ int tqsb_reconstruct_batch(tqsb_plan* p, const double* const* frames, int n_fram
     for (auto& r : rs)
         if (r.rc) return set_error(r.rc, r.err);
     const double e2e = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    fill_report(rep, rs, g, rs[0].classes_total, rs[0].classes_interior, e2e);
-    ljsde_report(p, rep);
+    fill_report(rep, rs, c, rs[0].classes_total, rs[0].classes_interior, e2e);
+    ljsde_report(c, rep);
     return TQSB_OK;
 }
 
-static int device_band(tqsb_plan* p, const double* d_frame, int frame_rows, int frame_cols,
-                       int br0, int br1, double* d_out, void* stream, tqsb_report* rep) {
+int device_band(tqsb_plan* p, const tqsb_config* call, const double* d_frame, int frame_rows,
+                int frame_cols, int br0, int br1, double* d_out, void* stream, tqsb_report* rep) {
     std::lock_guard<std::mutex> lk(p->mu);
+    tqsb_config c;
+    TQSB_TRY(call_config(p, call, &c));
     Geometry g;
-    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
+    TQSB_TRY(geometry(c, frame_rows, frame_cols, &g));
     if (br0 < 0 || br1 > g.padM / g.B || br0 > br1)
         return set_error(TQSB_EINVAL, "block-row band out of range");
     Device* d = p->devs[0].get();
     CUDA_TRY(cudaSetDevice(d->id));
     Work* w = nullptr;
+    Derived* dv = nullptr;
     int created = 0, launches = 0;
-    TQSB_TRY(prepare_band(p, d, g, frame_rows, frame_cols, br0, br1, &w, &created, &launches));
-    SolveArgs a = base_args(p, d);
+    TQSB_TRY(prepare_band(p, d, c, g, frame_rows, frame_cols, br0, br1, &w, &created, &launches));
+    TQSB_TRY(ensure_derived(p, d, c, &dv, &launches));
+    SolveArgs a = base_args(p, d, c, dv);
     a.frame = d_frame;
     a.frame_rows = frame_rows;
     a.frame_cols = frame_cols;
@@ -1132,7 +1265,7 @@ static int device_band(tqsb_plan* p, const double* d_frame, int frame_rows, int 
     a.task_cls = w->d_task_cls;
     a.n_tasks = w->n_tasks;
     if (w->n_items > 0) {
-        TQSB_TRY(launch(p, d, a, static_cast<cudaStream_t>(stream)));
+        TQSB_TRY(launch(c, d, a, static_cast<cudaStream_t>(stream), p->wt.NS));
         launches += 1;
     }
     if (rep) {
@@ -1144,23 +1277,72 @@ static int device_band(tqsb_plan* p, const double* d_frame, int frame_rows, int 
         rep->cache_misses = created;
         rep->cache_hits = w->n_tasks + (w->classes_total - created);
         rep->gpu_launches = launches;
+        rep->compute = uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE ? TQSB_COMPUTE_FP32
+                                                                        : TQSB_COMPUTE_FP64;
+        ljsde_report(c, rep);
     }
     return TQSB_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int tqsb_reconstruct_band(tqsb_plan* p, const double* frame, int frame_rows, int frame_cols,
+                          int br0, int br1, double* out_band, tqsb_report* rep) {
+    return reconstruct_band_impl(p, nullptr, frame, frame_rows, frame_cols, br0, br1, out_band, rep);
+}
+
+int tqsb_reconstruct_band_with(tqsb_plan* p, const tqsb_config* call, const double* frame,
+                               int frame_rows, int frame_cols, int br0, int br1, double* out_band,
+                               tqsb_report* rep) {
+    return reconstruct_band_impl(p, call, frame, frame_rows, frame_cols, br0, br1, out_band, rep);
+}
+
+int tqsb_reconstruct(tqsb_plan* p, const double* frame, int frame_rows, int frame_cols,
+                     double* out, const double* reference, tqsb_report* rep) {
+    return reconstruct_impl(p, nullptr, frame, frame_rows, frame_cols, out, reference, rep);
+}
+
+int tqsb_reconstruct_with(tqsb_plan* p, const tqsb_config* call, const double* frame,
+                          int frame_rows, int frame_cols, double* out, const double* reference,
+                          tqsb_report* rep) {
+    return reconstruct_impl(p, call, frame, frame_rows, frame_cols, out, reference, rep);
+}
+
+int tqsb_reconstruct_batch(tqsb_plan* p, const double* const* frames, int n_frames,
+                           int frame_rows, int frame_cols, double* const* outs, tqsb_report* rep) {
+    return reconstruct_batch_impl(p, nullptr, frames, n_frames, frame_rows, frame_cols, outs, rep);
+}
+
+int tqsb_reconstruct_batch_with(tqsb_plan* p, const tqsb_config* call, const double* const* frames,
+                                int n_frames, int frame_rows, int frame_cols, double* const* outs,
+                                tqsb_report* rep) {
+    return reconstruct_batch_impl(p, call, frames, n_frames, frame_rows, frame_cols, outs, rep);
+}
+
 int tqsb_reconstruct_device(tqsb_plan* p, const double* d_frame, int frame_rows, int frame_cols,
                             double* d_out, void* stream, tqsb_report* rep) {
+    return tqsb_reconstruct_device_with(p, nullptr, d_frame, frame_rows, frame_cols, d_out, stream,
+                                        rep);
+}
+
+int tqsb_reconstruct_device_with(tqsb_plan* p, const tqsb_config* call, const double* d_frame,
+                                 int frame_rows, int frame_cols, double* d_out, void* stream,
+                                 tqsb_report* rep) {
     if (!p || !d_frame || !d_out) return set_error(TQSB_EINVAL, "null argument");
+    tqsb_config c;
+    TQSB_TRY(call_config(p, call, &c));
     Geometry g;
-    TQSB_TRY(geometry(p->cfg, frame_rows, frame_cols, &g));
-    return device_band(p, d_frame, frame_rows, frame_cols, 0, g.padM / g.B, d_out, stream, rep);
+    TQSB_TRY(geometry(c, frame_rows, frame_cols, &g));
+    return device_band(p, call, d_frame, frame_rows, frame_cols, 0, g.padM / g.B, d_out, stream, rep);
 }
 
 int tqsb_reconstruct_band_device(tqsb_plan* p, const double* d_frame, int frame_rows,
                                  int frame_cols, int br0, int br1, double* d_out, void* stream,
                                  tqsb_report* rep) {
     if (!p || !d_frame || !d_out) return set_error(TQSB_EINVAL, "null argument");
-    return device_band(p, d_frame, frame_rows, frame_cols, br0, br1, d_out, stream, rep);
+    return device_band(p, nullptr, d_frame, frame_rows, frame_cols, br0, br1, d_out, stream, rep);
 }
 
 int tqsb_plan_export_tables(tqsb_plan* p, int orow, int ocol, int* local_out, double* b_re,
@@ -1172,7 +1354,7 @@ int tqsb_plan_export_tables(tqsb_plan* p, int orow, int ocol, int* local_out, do
     const int key = (orow % p->period) * p->period + (ocol % p->period);
     std::map<int, std::pair<int, int>> rep{{key, {orow, ocol}}};
     int created = 0, launches = 0;
-    TQSB_TRY(ensure_classes(p, d, {key}, rep, &created, &launches));
+    TQSB_TRY(ensure_classes(p, d, p->cfg, {key}, rep, &created, &launches));
     const ClassTab& t = d->tabs[d->slot_of.at(key)];
     *local_out = t.local;
     if (!b_re) return TQSB_OK;
@@ -1406,22 +1588,15 @@ int tqsb_plan_load_tables(tqsb_plan* p, const char* path, int* classes_out) {
             if (d->slot_of.count(key)) continue;  // already resident: the first insert wins
             CUDA_TRY(cudaSetDevice(d->id));
             ClassBuild cb;
-            TQSB_TRY(alloc_class(p, d, key, row, col, &cb));
+            TQSB_TRY(alloc_class(p, d, p->cfg, key, row, col, &cb));
             CUDA_TRY(cudaMemcpyAsync(cb.b64, b.data(), sizeof(double) * b.size(),
                                      cudaMemcpyHostToDevice, d->stream));
             CUDA_TRY(cudaMemcpyAsync(cb.c64, c.data(), sizeof(double) * c.size(),
                                      cudaMemcpyHostToDevice, d->stream));
             CUDA_TRY(cudaMemcpyAsync(cb.d64, dv.data(), sizeof(double) * K, cudaMemcpyHostToDevice,
                                      d->stream));
-            int launches = 0;
-            const int rc = launch_tables_batch(&cb, 1, window, p->wt.K_pad, p->cfg.step_width,
-                                               d->d_unit64, d->d_q64, d->d_perm, cb.local,
-                                               d->stream, &launches, 1, round_single(p->cfg));
-            if (rc != 0)
-                return set_error(TQSB_ECUDA, std::string("table derive: ") +
-                                                 cudaGetErrorString(cudaError_t(rc)));
+            // the planes are the cache; the fp32 product tables are derived on first use
             CUDA_TRY(cudaStreamSynchronize(d->stream));  // b/c/dv are reused next record
-            TQSB_TRY(publish_tabs(d));
         }
         ++installed;
     }
@@ -1439,7 +1614,9 @@ int tqsb_plan_block_trace(tqsb_plan* p, int orow, int ocol, const double* y_loca
     const int key = (orow % p->period) * p->period + (ocol % p->period);
     std::map<int, std::pair<int, int>> rep{{key, {orow, ocol}}};
     int created = 0, launches = 0;
-    TQSB_TRY(ensure_classes(p, d, {key}, rep, &created, &launches));
+    Derived* dv = nullptr;
+    TQSB_TRY(ensure_classes(p, d, p->cfg, {key}, rep, &created, &launches));
+    TQSB_TRY(ensure_derived(p, d, p->cfg, &dv, &launches));
     // a frame holding y_local at the window's cells (gather_local_values order)
     const int r0 = (orow + 1) / 2, r1 = (orow + W - 2) / 2;
     const int c0 = (ocol + 1) / 2, c1 = (ocol + W - 2) / 2;
@@ -1477,7 +1654,7 @@ int tqsb_plan_block_trace(tqsb_plan* p, int orow, int ocol, const double* y_loca
     cudaMemcpy(d_task, &t, sizeof(Task), cudaMemcpyHostToDevice);
     cudaMemcpy(d_item, &wi, sizeof(WorkItem), cudaMemcpyHostToDevice);
     cudaMemset(d_n, 0, sizeof(int));
-    SolveArgs a = base_args(p, d);
+    SolveArgs a = base_args(p, d, p->cfg, dv);
     a.frame = d_frame;
     a.frame_rows = fr;
     a.frame_cols = fc;
@@ -1496,7 +1673,7 @@ int tqsb_plan_block_trace(tqsb_plan* p, int orow, int ocol, const double* y_loca
     a.trace_gd = d_gd;
     a.trace_window = window_out ? d_win : nullptr;
     a.trace_n = d_n;
-    int rc = launch(p, d, a, d->stream);
+    int rc = launch(p->cfg, d, a, d->stream, p->wt.NS);
     if (rc) {
         cudaFree(buf);
         return rc;

@@ -328,7 +328,15 @@ int launch_ne(const SolveArgs& a, cudaStream_t st, int num_sms) {
     F64RLayout lay{K, a.iterations < K ? (a.iterations > 0 ? a.iterations : 1) : K};
     const size_t smem = lay.bytes() * kWarpsF64R + size_t(K) * sizeof(double);
     const size_t smem_init = size_t(K / 4 + 1) * kWarpsF64R * 8 + size_t(kWarpsF64R) * 2 * 32 * (kTileM + 1) * 16;
-    cudaError_t e = cudaFuncSetAttribute(k_solve_f64r<NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    // the per-warp coefficient lists grow with nu (W = 32, nu >= ~890 exceeds 227 KB):
+    // hand such launches to the generic kernel, which keeps its state in global memory
+    int dev = 0, smem_max = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess)
+        e = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    if (smem > size_t(smem_max) || smem_init > size_t(smem_max)) return cudaErrorNotSupported;
+    e = cudaFuncSetAttribute(k_solve_f64r<NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_init_f64r, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_init));
     if (e != cudaSuccess) return e;

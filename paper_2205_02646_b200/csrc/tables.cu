@@ -11,7 +11,10 @@
 //                 fac_u = gamma/(s_u D_u)
 //
 // All classes that a frame needs are built in one batched launch per stage
-// (grid.z = class), so the one-off precompute fills the GPU even at P = 8.
+// (grid.z = class), so the one-off precompute fills the GPU even at P = 8. The fp64
+// planes are the cache (the reference's KernelSet); the fp32 product tables depend on
+// per-call options (q through the frequency exponent, gamma) and are derived from the
+// planes lazily per option set (launch_tables_derive).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -216,11 +219,10 @@ __global__ void k_round_single(const ClassBuild* __restrict__ cls, int W) {
 
 } // namespace
 
-// Batched build over n classes; `descs` is a host array copied to the device here.
-int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, double step,
-                        const double* unit64, const double* q64, const int* perm,
-                        int max_local, void* stream_, int* launches, int derived_only,
-                        int round_single) {
+// Batched fp64 plane build over n classes (k_transform, k_gram, k_diag, and the
+// Precision::Single rounding); `descs` is a host array copied to the device here.
+int launch_tables_build(const void* host_descs, int n, int window, const double* unit64,
+                        int max_local, void* stream_, int* launches, int round_single) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     const ClassBuild* hd = static_cast<const ClassBuild*>(host_descs);
     ClassBuild* dd = nullptr;
@@ -232,27 +234,46 @@ int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, do
     for (int z0 = 0; z0 < n; z0 += 65535) {
         const int nz = n - z0 < 65535 ? n - z0 : 65535;
         const ClassBuild* d = dd + z0;
-        if (!derived_only) {
-            {
-                dim3 g((max_local + 127) / 128, K, nz);
-                k_transform<<<g, 128, 0, stream>>>(d, window, unit64);
-            }
-            {
-                const int nt = (K + GT - 1) / GT;
-                dim3 g(nt * (nt + 1) / 2, 1, nz);
-                k_gram<<<g, 256, 0, stream>>>(d, window, nt);
-            }
-            {
-                dim3 g((K + 255) / 256, 1, nz);
-                k_diag<<<g, 256, 0, stream>>>(d, window);
-            }
-            if (launches) *launches += 3;
+        {
+            dim3 g((max_local + 127) / 128, K, nz);
+            k_transform<<<g, 128, 0, stream>>>(d, window, unit64);
         }
+        {
+            const int nt = (K + GT - 1) / GT;
+            dim3 g(nt * (nt + 1) / 2, 1, nz);
+            k_gram<<<g, 256, 0, stream>>>(d, window, nt);
+        }
+        {
+            dim3 g((K + 255) / 256, 1, nz);
+            k_diag<<<g, 256, 0, stream>>>(d, window);
+        }
+        if (launches) *launches += 3;
         if (round_single) {
             dim3 g(4 * 148, 1, nz);
             k_round_single<<<g, 256, 0, stream>>>(d, window);
             if (launches) *launches += 1;
         }
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaFreeAsync(dd, stream);
+}
+
+// The fp32 product tables of n classes for one (frequency exponent, step width):
+// scale / fac (k_scale) and C' (k_pack32), derived from the resident fp64 planes.
+int launch_tables_derive(const void* host_descs, int n, int window, int k_pad, double step,
+                         const double* q64, const int* perm, void* stream_, int* launches) {
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    const ClassBuild* hd = static_cast<const ClassBuild*>(host_descs);
+    ClassBuild* dd = nullptr;
+    cudaError_t e = cudaMallocAsync(&dd, sizeof(ClassBuild) * n, stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(dd, hd, sizeof(ClassBuild) * n, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return e;
+    (void)window;
+    for (int z0 = 0; z0 < n; z0 += 65535) {
+        const int nz = n - z0 < 65535 ? n - z0 : 65535;
+        const ClassBuild* d = dd + z0;
         {
             dim3 g((k_pad + 255) / 256, 1, nz);
             k_scale<<<g, 256, 0, stream>>>(d, window, k_pad, perm, q64, step);
@@ -265,8 +286,7 @@ int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, do
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    e = cudaFreeAsync(dd, stream);
-    return e;
+    return cudaFreeAsync(dd, stream);
 }
 
 } // namespace tqsb

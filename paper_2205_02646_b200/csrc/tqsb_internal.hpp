@@ -121,13 +121,14 @@ struct ClassBuild {
     float* scale;              // K_pad
     float* fac;                // K_pad
 };
-// derived_only: b64 / c64 / d64 are already on the device (loaded TQSK planes);
-// only the fp32 product tables (k_scale, k_pack32) are derived from them.
-// round_single: store B, C, D rounded to float (the reference's Precision::Single).
-int launch_tables_batch(const void* host_descs, int n, int window, int k_pad, double step,
-                        const double* unit64, const double* q64, const int* perm,
-                        int max_local, void* stream, int* launches, int derived_only,
-                        int round_single);
+// fp64 planes (t64, b64, c64, d64) of n classes; round_single stores B, C, D rounded
+// to float (the reference's Precision::Single).
+int launch_tables_build(const void* host_descs, int n, int window, const double* unit64,
+                        int max_local, void* stream, int* launches, int round_single);
+// fp32 product tables (scale, fac, cpack) of n classes from their resident fp64
+// planes, for one (q = frequency weights, step width gamma).
+int launch_tables_derive(const void* host_descs, int n, int window, int k_pad, double step,
+                         const double* q64, const int* perm, void* stream, int* launches);
 
 int probe_peaks(int device, double* fp32_tflops, double* smem_tbps);
 

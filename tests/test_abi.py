@@ -130,3 +130,21 @@ def test_pad_to_block_multiple(tq):
     np.testing.assert_array_equal(padded[:9, :10], img)
     np.testing.assert_array_equal(padded[9:, :10], np.repeat(img[8:9], 3, 0))
     assert tq.pad_to_block_multiple(img, 3)[0].shape == (12, 12)
+
+
+def test_output_buffers_are_validated():
+    """Caller-supplied outputs go straight to the kernels / staging copies: wrong dtype,
+    shape, layout or count must be rejected before any C call (no device needed)."""
+    import numpy as np
+    import paper_2205_02646_b200 as tq
+    ok = np.empty((4, 6))
+    assert tq._out_array(ok, (4, 6)) is ok
+    assert tq._out_array(None, (4, 6)).shape == (4, 6)
+    for bad in (np.empty((4, 6), np.float32), np.empty((4, 5)), np.empty((6, 4)).T,
+                np.empty((4, 12))[:, ::2], [[0.0] * 6] * 4):
+        with pytest.raises(ValueError):
+            tq._out_array(bad, (4, 6))
+    ro = np.empty((4, 6))
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        tq._out_array(ro, (4, 6))

@@ -189,7 +189,8 @@ def test_noise_stress(tq, ref, need_gpu):
     rep = tq.reconstruct(frame, pat, tq.ReconstructionConfig(clip_output=False))
     r = _compare(rep.output, want, gt)
     print("noise:", r)
-    assert abs(r["dpsnr"]) <= 0.01, r
+    # the stress bound (test_gpu_fullsize.py::test_noise_stress_1mp)
+    assert abs(r["dpsnr"]) <= 0.01 and r["max_abs"] <= 0.1 and r["px_gt_1e4"] <= 0.02 * gt.size, r
 
 
 # ---------------------------------------------------------------- pipeline pins
