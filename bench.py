@@ -404,12 +404,16 @@ def main_ours(args):
             r = run_reference_sample(wl, args.cpu_sample_rows, 3, 1)
             cpu = {"value": round(r["value"], 5), "unit": "MP/s", "cores": r["cores"],
                    "kind": "reference", "sample": r["sample"], "cpu": cpu_model()}
-            # full frame: the parity reference and a check of the strip extrapolation
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "MP/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+        try:  # full frame: the parity reference and a check of the strip extrapolation
             want, rf = run_reference_full(wl, frame, pat.opaque, clip=True)
             cpu["full_frame_value"] = round(rf["value"], 5)
             cpu["full_frame_seconds"] = round(rf["wall_s"] - rf["warm_s"], 2)
             cpu["full_frame_warm_seconds"] = round(rf["warm_s"], 2)
-            cpu["strip_vs_full"] = round(r["value"] / rf["value"], 4)
+            if cpu.get("value"):
+                cpu["strip_vs_full"] = round(cpu["value"] / rf["value"], 4)
             d = np.abs(full - want)
             p_ours = 10 * np.log10(1.0 / np.mean((gt - full) ** 2))
             p_ref = 10 * np.log10(1.0 / np.mean((gt - want) ** 2))
@@ -419,13 +423,15 @@ def main_ours(args):
                       "px_gt_1e4": int((d > 1e-4).sum()), "px": int(d.size),
                       "gate": "max_abs <= 1e-2 and |dpsnr| <= 0.01 dB",
                       "pass": bool(d.max() <= 1e-2 and abs(p_ours - p_ref) <= 0.01)}
-            # per core (threads = 1): the paper's protocol, on a 16-row strip
-            r1 = run_reference_sample(wl, 16, 1, 1, threads=1)
+        except Exception as e:  # pragma: no cover
+            parity = {"unavailable": str(e)}
+        try:  # per core (threads = 1): the paper's protocol, on a 32-row strip (W = 32)
+            r1 = run_reference_sample(wl, 32, 1, 1, threads=1)
             cpu["per_core_value"] = round(r1["value"], 6)
             cpu["per_core_sample"] = r1["sample"] + ", threads = 1"
         except Exception as e:  # pragma: no cover
-            cpu = {"value": None, "unit": "MP/s", "cores": None, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+            cpu["per_core_value"] = None
+            cpu["per_core_sample"] = f"unavailable: {e}"
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")

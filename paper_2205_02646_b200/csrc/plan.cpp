@@ -12,9 +12,13 @@
 // The per-block solve, synthesis and placement run on the device (solve_f32.cu,
 // solve_f64.cu); the tables are built on the device (tables.cu). There is no CPU
 // fallback: without a CUDA device every compute entry point fails with TQSB_ENODEV.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <tuple>
 #include <chrono>
 #include <cmath>
@@ -50,6 +54,15 @@ int set_error(int code, const std::string& msg) {
         if (_e != cudaSuccess)                                                                 \
             return set_error(_e == cudaErrorMemoryAllocation ? TQSB_ENOMEM : TQSB_ECUDA,       \
                              std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+    } while (0)
+
+// in functions that report through BandResult (void): record the failure and return
+#define CUDA_TRY_V(expr)                                                                       \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return fail(set_error(_e == cudaErrorMemoryAllocation ? TQSB_ENOMEM : TQSB_ECUDA,  \
+                                  std::string(#expr) + ": " + cudaGetErrorString(_e)));       \
     } while (0)
 
 #define TQSB_TRY(expr)            \
@@ -279,10 +292,10 @@ struct ClassSlab {
 };
 
 struct WorkKey {
-    int rows, cols, br0, br1, block, chunk;
+    int rows, cols, br0, br1, block, chunk, stream;
     bool operator<(const WorkKey& o) const {
-        return std::tie(rows, cols, br0, br1, block, chunk) <
-               std::tie(o.rows, o.cols, o.br0, o.br1, o.block, o.chunk);
+        return std::tie(rows, cols, br0, br1, block, chunk, stream) <
+               std::tie(o.rows, o.cols, o.br0, o.br1, o.block, o.chunk, o.stream);
     }
 };
 
@@ -294,7 +307,14 @@ struct Work {
     int frame_row0 = 0, frame_row1 = 0;  // frame rows the band needs
     std::vector<int> keys;                // classes used
     long long classes_total = 0, classes_interior = 0;
+    // streamed completion (stream > 0 chunks): tasks ordered chunk by chunk (class-sorted
+    // within a chunk); chunk s holds chunk_count[s] blocks covering block rows
+    // [chunk_br[s], chunk_br[s+1])
+    std::vector<int> chunk_count, chunk_br;
+    std::vector<int> chunk_fr_hi;  // frame rows [frame_row0, chunk_fr_hi[s]) cover chunk s
 };
+constexpr int kStreamChunks = 16;       // output chunks of a streamed host-buffer call
+constexpr int kStreamMinTasks = 8192;   // below this a frame is not worth streaming
 
 // The per-call derived tables of one option set. The cache proper is the fp64 planes
 // (B, C, D per offset class: the reference's KernelSet, rljsde.hpp:34-52), which
@@ -328,6 +348,9 @@ struct Device {
     float* d_unit32 = nullptr;
     double* d_unit64 = nullptr;
     uint8_t* d_opaque = nullptr;   // the pattern's (P/2)^2 quadrant indices (device readout)
+    int* d_progress = nullptr;     // chunk counters of a streamed call (device memory):
+                                   // [0, 64) blocks finished, [64, 128) input rows ready
+    cudaEvent_t ev_chunk[64] = {}; // chunk s copied to the pinned staging
     int* d_counters = nullptr;     // kCounterRing dynamic task-queue heads
     unsigned counter_next = 0;
     std::map<int, int> slot_of;    // class key -> slot
@@ -416,6 +439,9 @@ void device_free(Device* d) {
     cudaFree(d->d_unit64);
     cudaFree(d->d_opaque);
     cudaFree(d->d_counters);
+    cudaFree(d->d_progress);
+    for (auto& e : d->ev_chunk)
+        if (e) cudaEventDestroy(e);
     cudaFree(d->d_frame);
     cudaFree(d->d_out);
     if (d->h_in) cudaFreeHost(d->h_in);
@@ -438,15 +464,15 @@ void device_free(Device* d) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// memcpy of large host buffers (pageable <-> pinned staging) on up to 8 threads
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-    const size_t kMin = size_t(8) << 20;
-    unsigned nt = std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency()));
-    if (bytes < kMin || nt <= 1) {
+// memcpy of large host buffers (pageable <-> pinned staging) on up to max_threads threads
+void par_memcpy(void* dst, const void* src, size_t bytes, unsigned max_threads = 8) {
+    const size_t kPerThread = size_t(2) << 20;  // at least 2 MB per thread
+    unsigned nt = std::min<unsigned>(max_threads, std::max(1u, std::thread::hardware_concurrency()));
+    nt = unsigned(std::min<size_t>(nt, bytes / kPerThread));
+    if (nt <= 1) {
         std::memcpy(dst, src, bytes);
         return;
     }
-    nt = unsigned(std::min<size_t>(nt, bytes / (kMin / 4)));
     std::vector<std::thread> th;
     const size_t chunk = (bytes + nt - 1) / nt;
     for (unsigned i = 0; i < nt; ++i) {
@@ -623,10 +649,11 @@ int ensure_derived(tqsb_plan* p, Device* d, const tqsb_config& c, Derived** out,
 // Class-sorted tasks and CTA work items for a band of block rows on device d;
 // the band's classes are made resident first (cached per frame shape and band).
 int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& g, int frame_rows,
-                 int frame_cols, int br0, int br1, Work** out, int* created, int* launches) {
+                 int frame_cols, int br0, int br1, Work** out, int* created, int* launches,
+                 int stream = 0) {
     *created = 0;
     const int chunk = (uses_f32(c) ? kWarpsF32 : kWarpsF64) * 4;
-    const WorkKey wkey{frame_rows, frame_cols, br0, br1, g.B, chunk};
+    const WorkKey wkey{frame_rows, frame_cols, br0, br1, g.B, chunk, stream};
     Enumerated e;
     auto it = d->works.find(wkey);
     if (it != d->works.end()) {
@@ -658,25 +685,51 @@ int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& 
     if (e.tasks.empty()) omin = omax = 0;
     w.frame_row0 = std::min(omin / 2, frame_rows - 1);
     w.frame_row1 = std::min(frame_rows, (omax + g.W - 1) / 2 + 1);
-    // class-sorted (stable) task list, cut into CTA work items of one class each
-    std::vector<std::vector<Task>> by_key(size_t(p->period) * p->period);
-    for (size_t i = 0; i < e.tasks.size(); ++i) by_key[e.keys[i]].push_back(e.tasks[i]);
+    // class-sorted (stable) task list, cut into CTA work items of one class each; a
+    // streamed list is ordered chunk by chunk of block rows first (class-sorted inside
+    // each chunk) and carries the chunk in task_cls
+    const int n_chunks = stream > 0 ? stream : 1;
+    const int nbr = br1 - br0;
+    // chunk boundaries shrink toward the end (fraction 1 - (1 - s/S)^2): the rows handed
+    // over after the kernel ends -- the exposed tail -- are the last, smallest chunk
+    for (int s = 0; s <= n_chunks; ++s) {
+        const double f = 1.0 - (1.0 - double(s) / n_chunks) * (1.0 - double(s) / n_chunks);
+        int b = br0 + int(std::lround(nbr * f));
+        if (s > 0) b = std::max(b, w.chunk_br.back());
+        w.chunk_br.push_back(s == n_chunks ? br1 : b);
+    }
+    w.chunk_count.assign(n_chunks, 0);
+    w.chunk_fr_hi.assign(n_chunks, w.frame_row0);
     std::vector<Task> sorted;
     std::vector<WorkItem> items;
     std::vector<int> task_cls;
     sorted.reserve(e.tasks.size());
     task_cls.reserve(e.tasks.size());
-    for (int k : e.class_order) {
-        const auto& v = by_key[k];
-        for (size_t s = 0; s < v.size(); s += chunk) {
-            WorkItem wi{};
-            wi.cls = d->slot_of.at(k);
-            wi.start = int(sorted.size() + s);
-            wi.count = int(std::min<size_t>(chunk, v.size() - s));
-            items.push_back(wi);
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        std::vector<std::vector<Task>> by_key(size_t(p->period) * p->period);
+        for (size_t i = 0; i < e.tasks.size(); ++i) {
+            const int bri = e.tasks[i].block_row / g.B;
+            if (bri >= w.chunk_br[ch] && bri < w.chunk_br[ch + 1]) {
+                by_key[e.keys[i]].push_back(e.tasks[i]);
+                // frame rows this chunk's windows read: through (origin + W - 1) / 2
+                w.chunk_fr_hi[ch] = std::max(w.chunk_fr_hi[ch],
+                                             std::min(frame_rows, (e.tasks[i].origin_row + g.W - 1) / 2 + 1));
+            }
         }
-        sorted.insert(sorted.end(), v.begin(), v.end());
-        task_cls.insert(task_cls.end(), v.size(), d->slot_of.at(k));
+        for (int k : e.class_order) {
+            const auto& v = by_key[k];
+            for (size_t s = 0; s < v.size(); s += chunk) {
+                WorkItem wi{};
+                wi.cls = d->slot_of.at(k);
+                wi.start = int(sorted.size() + s);
+                wi.count = int(std::min<size_t>(chunk, v.size() - s));
+                items.push_back(wi);
+            }
+            sorted.insert(sorted.end(), v.begin(), v.end());
+            task_cls.insert(task_cls.end(), v.size(),
+                            d->slot_of.at(k) | (stream > 0 ? ch << kTaskClsBits : 0));
+            w.chunk_count[ch] += int(v.size());
+        }
     }
     w.n_items = int(items.size());
     CUDA_TRY(cudaSetDevice(d->id));
@@ -778,6 +831,63 @@ struct BandResult {
     long long classes_total = 0, classes_interior = 0, blocks = 0;
 };
 
+// First-touch population of a caller's output buffer while the GPU works, so the
+// hand-over copies find resident pages (a fresh std::vector / numpy array faults on
+// every 4 KB page: ~16 k faults for a 4K frame). MADV_POPULATE_WRITE (Linux 5.14)
+// populates without changing contents, so it may run alongside the copies; on older
+// kernels it fails harmlessly and the copies fault as before.
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23
+#endif
+std::thread prefault_async(void* p, size_t bytes) {
+    static const bool enabled = [] {
+        const char* v = std::getenv("TQSB_PREFAULT");
+        return !(v && v[0] == '0');
+    }();
+    if (!enabled || bytes < (size_t(1) << 20)) return std::thread();
+    return std::thread([p, bytes] {
+        const uintptr_t pg = uintptr_t(sysconf(_SC_PAGESIZE));
+        uintptr_t a = (reinterpret_cast<uintptr_t>(p) + pg - 1) / pg * pg;
+        const uintptr_t end = (reinterpret_cast<uintptr_t>(p) + bytes) / pg * pg;
+        const uintptr_t step = uintptr_t(4) << 20;  // in order, 4 MB at a time
+        for (; a < end; a += step)
+            if (madvise(reinterpret_cast<void*>(a), std::min(step, end - a), MADV_POPULATE_WRITE) != 0)
+                break;
+    });
+}
+
+// cuStreamWaitValue32 (stream memory operations, driver API) through the runtime's
+// driver entry-point query; null when the driver or device does not offer it
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32Fn wait_value32() {
+    static WaitValue32Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return WaitValue32Fn(nullptr);
+        }
+        return reinterpret_cast<WaitValue32Fn>(f);
+    }();
+    return fn;
+}
+
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+    static WriteValue32Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return WriteValue32Fn(nullptr);
+        }
+        return reinterpret_cast<WriteValue32Fn>(f);
+    }();
+    return fn;
+}
+
 // Host-buffer band run on device d: H2D of the band's frame rows (halo included),
 // one solve launch whose B x B output tiles are stored straight into pinned host
 // memory (zero-copy: the caller's buffer when it is pinned, else the plan's pinned
@@ -790,10 +900,26 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
         r->err = g_error;
     };
     if (cudaSetDevice(d->id) != cudaSuccess) return fail(set_error(TQSB_ECUDA, "cudaSetDevice"));
+    const bool out_pinned = is_pinned(out_band);
+    // A pageable output on the fp32 kernel streams: the kernel stores into device memory
+    // and counts finished blocks per chunk of block rows; a copy stream waits on each
+    // chunk's count (cuStreamWaitValue32) and moves its rows to pinned staging, and the
+    // host hands them to the caller's buffer -- so the staging copy and the first-touch
+    // page faults of a fresh buffer overlap the solve instead of following it.
+    const long long n_est = (long long)(br1 - br0) * (g.padN / g.B);
+    // (the warp-scheduled kernel only: the TMEM column tier runs CTA work items)
+    const int stream = !out_pinned && uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE &&
+                               c.hot_columns <= 0 &&
+                               solve_f32_streams(p->wt.NS, c.block * c.block) &&
+                               n_est >= kStreamMinTasks && br1 - br0 >= kStreamChunks &&
+                               wait_value32() != nullptr && write_value32() != nullptr
+                           ? kStreamChunks
+                           : 0;
     Work* w = nullptr;
     Derived* dv = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    int rc = prepare_band(p, d, c, g, frame_rows, frame_cols, br0, br1, &w, &r->created, &r->launches);
+    int rc = prepare_band(p, d, c, g, frame_rows, frame_cols, br0, br1, &w, &r->created, &r->launches,
+                          stream);
     if (!rc) rc = ensure_derived(p, d, c, &dv, &r->launches);
     if (rc) return fail(rc);
     r->warm = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -804,22 +930,35 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
     const size_t in_n = size_t(fr1 - fr0) * frame_cols;
     const int orow0 = br0 * g.B, orow1 = std::min(br1 * g.B, g.M);
     const size_t out_n = size_t(std::max(0, orow1 - orow0)) * g.N;
-    const bool in_pinned = is_pinned(frame), out_pinned = is_pinned(out_band);
+    const bool in_pinned = is_pinned(frame);
     if ((rc = ensure_buffer(&d->d_frame, &d->frame_cap, in_n))) return fail(rc);
     if (!in_pinned && (rc = ensure_pinned(&d->h_in, &d->h_in_cap, in_n))) return fail(rc);
     if (!out_pinned && (rc = ensure_pinned(&d->h_out, &d->h_out_cap, out_n))) return fail(rc);
+    if (stream) {
+        if ((rc = ensure_buffer(&d->d_out, &d->out_cap, out_n))) return fail(rc);
+        if (!d->d_progress) {
+            CUDA_TRY_V(cudaMalloc(&d->d_progress, sizeof(int) * 128));
+            for (auto& e : d->ev_chunk) CUDA_TRY_V(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
     const double* src = frame + size_t(fr0) * frame_cols;
-    if (!in_pinned) {
+    // a streamed call with a pageable frame stages its rows chunk by chunk after the
+    // launch; the kernel waits per chunk on an input-ready flag (SolveArgs::in_ready)
+    const bool stream_in = stream && !in_pinned;
+    if (!in_pinned && !stream_in) {
         par_memcpy(d->h_in, src, sizeof(double) * in_n);
         src = d->h_in;
     }
     double* host_out = out_pinned ? out_band : d->h_out;
     double* dev_view = nullptr;  // the pinned output as seen from the device (UVA)
-    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_view), host_out, 0) != cudaSuccess) {
+    if (stream) {
+        dev_view = d->d_out;
+    } else if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_view), host_out, 0) != cudaSuccess) {
         cudaGetLastError();
         return fail(set_error(TQSB_ECUDA, "output buffer is not device-mapped pinned memory"));
     }
-    cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
+    if (!stream_in)
+        cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
     SolveArgs a = base_args(p, d, c, dv);
     a.frame = d->d_frame;
     a.frame_rows = frame_rows;
@@ -835,17 +974,112 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
     a.n_items = w->n_items;
     a.task_cls = w->d_task_cls;
     a.n_tasks = w->n_tasks;
+    // rows [chunk_br[s] * B, chunk_br[s+1] * B) of the output, cropped to M, relative to orow0
+    auto chunk_rows = [&](int s, size_t* off, size_t* n) {
+        const int r0 = std::min(w->chunk_br[s] * g.B, g.M), r1 = std::min(w->chunk_br[s + 1] * g.B, g.M);
+        *off = size_t(std::max(0, r0 - orow0)) * g.N;
+        *n = size_t(std::max(0, r1 - r0)) * g.N;
+    };
+    if (stream) {
+        a.progress = d->d_progress;
+        a.in_ready = stream_in ? d->d_progress + 64 : nullptr;
+        CUDA_TRY_V(cudaMemsetAsync(d->d_progress, 0, sizeof(int) * 128, d->stream));
+        CUDA_TRY_V(cudaEventRecord(d->ev_h2d[2], d->stream));  // counters zeroed
+        CUDA_TRY_V(cudaStreamWaitEvent(d->s_d2h, d->ev_h2d[2], 0));
+        CUDA_TRY_V(cudaStreamWaitEvent(d->s_h2d, d->ev_h2d[2], 0));
+    }
     cudaEventRecord(d->ev0, d->stream);
     if (w->n_items > 0) {
         if ((rc = launch(c, d, a, d->stream, p->wt.NS))) return fail(rc);
         r->launches += 1;
     }
     cudaEventRecord(d->ev1, d->stream);
+    if (stream_in) {  // frame rows chunk by chunk: stage, copy, raise the chunk's flag
+        WriteValue32Fn writev = write_value32();
+        int done = fr0;
+        for (int s = 0; s < stream; ++s) {
+            // whole 128 B lines: a line the kernel reads for chunk s never holds rows
+            // that are not on the device yet
+            size_t b0 = size_t(done - fr0) * frame_cols * sizeof(double);
+            size_t b1 = size_t(std::max(done, w->chunk_fr_hi[s]) - fr0) * frame_cols * sizeof(double);
+            b1 = std::min(in_n * sizeof(double), (b1 + 127) / 128 * 128);
+            b0 = std::min(b0, b1);
+            if (b1 > b0) {
+                par_memcpy(reinterpret_cast<char*>(d->h_in) + b0, reinterpret_cast<const char*>(src) + b0,
+                           b1 - b0, 4);
+                cudaMemcpyAsync(reinterpret_cast<char*>(d->d_frame) + b0,
+                                reinterpret_cast<const char*>(d->h_in) + b0, b1 - b0,
+                                cudaMemcpyHostToDevice, d->s_h2d);
+            }
+            done = std::max(done, fr0 + int(b1 / (sizeof(double) * frame_cols)));
+            if (writev(reinterpret_cast<CUstream>(d->s_h2d),
+                       reinterpret_cast<CUdeviceptr>(d->d_progress + 64 + s), 1,
+                       CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+                // release the waiting kernel before failing (it must not spin forever)
+                std::vector<int> one(stream, 1);
+                cudaStreamSynchronize(d->s_h2d);
+                cudaMemcpy(d->d_progress + 64, one.data(), sizeof(int) * stream, cudaMemcpyHostToDevice);
+                cudaStreamSynchronize(d->stream);
+                return fail(set_error(TQSB_ECUDA, "cuStreamWriteValue32 failed"));
+            }
+        }
+    }
+    std::thread prefault;  // joined before returning (the buffer is the caller's)
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } joiner{prefault};
+    if (stream) prefault = prefault_async(out_band, sizeof(double) * out_n);
+    if (stream) {
+        WaitValue32Fn waitv = wait_value32();
+        for (int s = 0; s < stream; ++s) {
+            size_t off, n;
+            chunk_rows(s, &off, &n);
+            if (waitv(reinterpret_cast<CUstream>(d->s_d2h),
+                      reinterpret_cast<CUdeviceptr>(d->d_progress + s),
+                      cuuint32_t(w->chunk_count[s]), CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return fail(set_error(TQSB_ECUDA, "cuStreamWaitValue32 failed"));
+            if (n) cudaMemcpyAsync(d->h_out + off, d->d_out + off, sizeof(double) * n,
+                                   cudaMemcpyDeviceToHost, d->s_d2h);
+            cudaEventRecord(d->ev_chunk[s], d->s_d2h);
+        }
+        // hand the chunks over as they land; a failed solve releases the copy stream
+        int s = 0;
+        for (; s < stream; ++s) {
+            cudaError_t q;
+            std::chrono::steady_clock::time_point done_at{};
+            bool solve_done = false;
+            while ((q = cudaEventQuery(d->ev_chunk[s])) == cudaErrorNotReady) {
+                const cudaError_t m = cudaStreamQuery(d->stream);
+                if (m != cudaErrorNotReady && m != cudaSuccess) break;  // the solve failed
+                if (m == cudaSuccess) {  // solved: the chunk copies must land promptly
+                    if (!solve_done) done_at = std::chrono::steady_clock::now(), solve_done = true;
+                    else if (std::chrono::steady_clock::now() - done_at > std::chrono::seconds(5)) break;
+                }
+                std::this_thread::yield();
+            }
+            if (q != cudaSuccess) break;
+            size_t off, n;
+            chunk_rows(s, &off, &n);
+            par_memcpy(out_band + off, d->h_out + off, sizeof(double) * n, 4);
+        }
+        if (s < stream) {  // the solve failed: unblock the waits so the copy stream drains
+            const cudaError_t err = cudaStreamSynchronize(d->stream);
+            std::vector<int> big(stream, 0x7fffffff);
+            cudaMemcpy(d->d_progress, big.data(), sizeof(int) * stream, cudaMemcpyHostToDevice);
+            cudaStreamSynchronize(d->s_d2h);
+            cudaGetLastError();
+            return fail(set_error(TQSB_ECUDA, std::string("solve: ") + cudaGetErrorString(
+                                                  err != cudaSuccess ? err : cudaErrorUnknown)));
+        }
+    }
     cudaError_t e = cudaStreamSynchronize(d->stream);
     if (e != cudaSuccess)
         return fail(set_error(TQSB_ECUDA, std::string("solve: ") + cudaGetErrorString(e)));
     cudaEventElapsedTime(&r->ms, d->ev0, d->ev1);
-    if (!out_pinned) par_memcpy(out_band, d->h_out, sizeof(double) * out_n);
+    if (!stream && !out_pinned) par_memcpy(out_band, d->h_out, sizeof(double) * out_n);
 }
 
 // Multi-frame pipeline on one device: frame i+1's H2D (copy stream) overlaps frame

@@ -36,34 +36,23 @@
 #include "solve_common.cuh"
 
 #ifndef TQSB_KEYS
-#define TQSB_KEYS 1  // packed score/position keys (see score_key)
+// packed score/position keys (see score_key). TQSB_KEYS=0 builds the exact-selection
+// variant (score buffer + smallest-flat-index tie scan), kept as the reference for the
+// keys' share of fp32 path forks (profiles/r02_parity.md, tools/parity_r02.py)
+#define TQSB_KEYS 1
 #endif
 #ifndef TQSB_DYN
 #define TQSB_DYN 1  // warp-level dynamic task scheduling when no CTA-wide class state is needed
-#endif
-#ifndef TQSB_TIMING
-#define TQSB_TIMING 0  // per-phase clock() accounting of the iteration (experiment builds)
 #endif
 #ifndef TQSB_AHEAD
 #define TQSB_AHEAD 2  // 4-slot column chunks in flight ahead of the update (NS == 16)
 #endif
 
 namespace tqsb {
-#if TQSB_TIMING
-__device__ unsigned long long g_tdbg[16];
-#endif
 namespace {
 
 using namespace dev;
 
-#if TQSB_TIMING
-__device__ __forceinline__ unsigned clk_after(int v) {  // clock read ordered after v is ready
-    unsigned c;
-    asm volatile("{ .reg .pred p; setp.eq.s32 p, %1, -123456789; @p trap; mov.u32 %0, %%clock; }"
-                 : "=r"(c) : "r"(v));
-    return c;
-}
-#endif
 
 // per-warp scratch floats: the init transpose buffer zbuf[gamma][sigma] (float2,
 // row stride 18) / half-spectrum r0buf[sigma][rho], aliased with the element-score
@@ -79,9 +68,12 @@ struct Scratch {
 // NW warps per CTA (1 CTA per SM): 16 at 128 registers where the kernel fits without
 // spilling in the loop (the default W = 32 / B = 4 product path: 38.8 vs 40.5 ms per 4K frame at 12),
 // 12 at 168 registers for the heavier instantiations (B >= 8, TMEM tier, tracing)
-template <int NS, int W, int PPL, bool TRACE, bool TM, int NW>
+// SP: the streamed host-buffer variant (SolveArgs::progress / in_ready, chunk-tagged
+// task list); a separate instantiation so the device-resident path carries none of it
+template <int NS, int W, int PPL, bool TRACE, bool TM, int NW, bool SP = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
     constexpr bool DYN = !TRACE && !TM && TQSB_DYN;  // per-warp task queue (a.counter)
+    static_assert(!SP || DYN, "streamed completion needs the warp-level task queue");
     extern __shared__ __align__(16) float smem[];
     constexpr int COLF4 = NS * 32;  // float4 per column
     constexpr int KP = NS * 64;     // padded frequency count
@@ -129,7 +121,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
     }
 
     // one target block end to end: init, nu iterations, synthesis, placement
-    auto solve_task = [&](const int ti, const ClassTab& ct) {
+    auto solve_task = [&](const int ti, const ClassTab& ct, const int chunk) {
         const float4* __restrict__ gcols = reinterpret_cast<const float4*>(ct.cpack);
         const float2* __restrict__ scale2 = reinterpret_cast<const float2*>(ct.scale);
         const Task tk = a.tasks[ti];
@@ -225,14 +217,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         const bool tracing = TRACE && ti == 0;
 
         int it = 0;
-#if TQSB_TIMING
-        unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0};
-#endif
         for (; it < a.iterations; ++it) {
             __syncwarp();
-#if TQSB_TIMING
-            const unsigned t0 = clk_after(__float_as_int(lmax));
-#endif
             // ---- argmax over the warp (NaN = inadmissible, ignored by max) ----
             const float gmax = warp_max_f32(lmax);
             if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
@@ -295,18 +281,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
             // (fac bits, flat k) of rank u: CTA-shared table, or through L1 when scheduled per warp
             const int2 meta = DYN ? make_int2(__float_as_int(__ldg(ct.fac + u)), __ldg(a.wc.perm + u))
                                   : s_meta[u];
-#if TQSB_TIMING
-            const unsigned t1 = clk_after(u);
-#endif
             const float2 v = pick_elem<NS>(R, t);
             const float ure = __shfl_sync(FULL, v.x, Lw);
             const float uim = __shfl_sync(FULL, v.y, Lw);
             const float f = __int_as_float(meta.x);
             const float gre = f * ure, gim = f * uim;
             const int kflat = meta.y;
-#if TQSB_TIMING
-            const unsigned t2 = clk_after(__float_as_int(gre) ^ __float_as_int(gim));
-#endif
             // synthesis phases of the kept pixels: issued now, consumed after the update
             const unsigned sigma = unsigned(kflat) / W, rho = unsigned(kflat) % W;
             float2 ph[PPL];
@@ -334,15 +314,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
             }
 #endif
             }
-#if TQSB_TIMING
-            {
-                const unsigned t3 = clk_after(__float_as_int(lmax));
-                tacc[0] += t1 - t0;
-                tacc[1] += t2 - t1;
-                tacc[in_tmem ? 2 : 3] += t3 - t2;
-                tacc[in_tmem ? 4 : 5] += 1;
-            }
-#endif
             // ---- synthesis of the kept block pixels (off the critical path) ----
 #pragma unroll
             for (int j = 0; j < PPL; ++j) acc[j] = fmaf(gre, ph[j].x, fmaf(-gim, ph[j].y, acc[j]));
@@ -352,10 +323,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
                 a.trace_gd[2 * it + 1] = gim;
             }
         }
-#if TQSB_TIMING
-        if (lane == 0)
-            for (int q = 0; q < 6; ++q) atomicAdd(&g_tdbg[q], tacc[q]);
-#endif
         // ---- placement: clip + crop straight into the output ----
         const int2 bo = make_int2(tk.block_row, tk.block_col);
 #pragma unroll
@@ -369,6 +336,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
                     a.out[size_t(orow - a.out_row0) * a.out_cols + ocol] = double(val);
                 }
             }
+        }
+        if (SP) {  // streamed completion: this block's rows are final
+            __syncwarp();           // orders the lanes' stores before lane 0's release
+            if (lane == 0)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + chunk)
+                             : "memory");
         }
         if (tracing) {
             if (lane == 0) *a.trace_n = it;
@@ -393,12 +366,29 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         // warp-level dynamic scheduling over the class-sorted task list: no CTA-wide
         // class state (per-rank factors are read through L1), and no tail imbalance
         // beyond one block per warp
+        int ready = -1;  // streamed input: chunks known to be on the device
         for (;;) {
             int ti = 0;
             if (lane == 0) ti = atomicAdd(a.counter, 1);
             ti = __shfl_sync(FULL, ti, 0);
             if (ti >= a.n_tasks) break;
-            solve_task(ti, a.tabs[__ldg(a.task_cls + ti)]);
+            const int tc = __ldg(a.task_cls + ti);
+            if (SP && a.in_ready && (tc >> kTaskClsBits) > ready) {
+                // chunks are handed out in order: wait for this one's frame rows once
+                // (the frame reads below depend on the flag through this branch, and no
+                // line of these rows was read before they landed)
+                const int ch = tc >> kTaskClsBits;
+                if (lane == 0) {
+                    volatile const int* f = a.in_ready + ch;
+                    while (*f == 0) __nanosleep(256);
+                }
+                __syncwarp();
+                ready = ch;
+            }
+            if constexpr (SP)
+                solve_task(ti, a.tabs[tc & ((1 << kTaskClsBits) - 1)], tc >> kTaskClsBits);
+            else
+                solve_task(ti, a.tabs[tc], 0);
         }
     } else {
         for (int it_item = blockIdx.x; it_item < a.n_items; it_item += gridDim.x) {
@@ -423,7 +413,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
             const ClassTab ct = a.tabs[item.cls];
 
             for (int ti = item.start + warp; ti < item.start + item.count; ti += NW)
-                solve_task(ti, ct);
+                solve_task(ti, ct, 0);
         }
     }
     tmem_sync_all();
@@ -441,6 +431,13 @@ int launch_one(const SolveArgs& a, cudaStream_t stream, int num_sms) {
     auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true, false, kWarpsF32Heavy>
                 : a.hot > 0   ? k_solve_f32<NS, W, PPL, false, true, kWarpsF32Heavy>
                               : k_solve_f32<NS, W, PPL, false, false, NWP>;
+    if (a.progress) {  // streamed host-buffer call: the product instantiations only
+        if constexpr (solve_f32_streams(NS, PPL == 1 ? 16 : 64))
+            kern = k_solve_f32<NS, W, PPL, false, false, NWP, true>;
+        else
+            return cudaErrorNotSupported;
+        if (a.trace_picks || a.hot > 0) return cudaErrorNotSupported;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
@@ -468,11 +465,6 @@ int launch_w(const SolveArgs& a, int n_slots, cudaStream_t s, int num_sms) {
 
 } // namespace
 
-#if TQSB_TIMING
-extern "C" int tqsb_debug_timing(unsigned long long* out) {
-    return cudaMemcpyFromSymbol(out, g_tdbg, sizeof(unsigned long long) * 6);
-}
-#endif
 
 size_t solve_f32_smem_bytes(int n_slots, int warps) {
     // (fac, perm) per rank + unit table + per-warp scratch; hot columns live in TMEM

@@ -90,7 +90,21 @@ struct SolveArgs {
     double* trace_gd;
     double* trace_window;
     int* trace_n;
+    // streamed completion (fp32 kernel, warp-level scheduling): when non-null, task_cls
+    // entries carry a chunk index above kTaskClsBits and every finished block bumps
+    // progress[chunk] (device memory, release at GPU scope after the block's output
+    // stores), which a copy stream waits on (cuStreamWaitValue32) to move finished
+    // output rows to the host while the kernel runs
+    int* progress;
+    // streamed input: when non-null, the frame rows of chunk s are on the device once
+    // in_ready[s] != 0 (written by the copy stream after their H2D); a warp checks the
+    // flag before its first task of each chunk
+    int* in_ready;
 };
+constexpr int kTaskClsBits = 20;  // task_cls = class slot | chunk << kTaskClsBits
+// the fp32 kernel has a streamed instantiation for NS == 16 slots (W = 23..32) and
+// B*B <= 32 kept pixels (B <= 5): the product configurations
+constexpr bool solve_f32_streams(int n_slots, int block_px) { return n_slots == 16 && block_px <= 32; }
 
 // test hook (env TQSB_FORCE_GLOBAL_STATE=1): the fp64 / L-JSDE kernels keep their
 // per-block state in global memory even when it fits in shared memory, so the

@@ -85,18 +85,25 @@ def test_criterion6_window_scaling(tq, need_gpu, runs):
     r0 = runs[0]
     pat = tq.generate_pattern(7, 32)
     l16 = _run(tq, pat, r0["frame"], _protocol(tq, tq.ALGO_LJSDE, 16))
-    rl16 = _run(tq, pat, r0["frame"], _protocol(tq, tq.ALGO_RLJSDE, 16, tq.COMPUTE_FP64))
-    # the fp32 kernel on the 512^2 image: 1,024 blocks leave the B200's 2,368 warps half
-    # idle, which measures one block's latency chain instead of the per-block cost
+    # the RL-JSDE kernels on the 512^2 image: 1,024 blocks leave the B200's warps mostly
+    # idle and the few-ms launches are dominated by fixed costs (the fp64 ratio on 128^2
+    # ranged 1.6-7.3 run to run); per-block time = the best of three calls
     r5 = runs[5]
-    f16 = _run(tq, pat, r5["frame"], _protocol(tq, tq.ALGO_RLJSDE, 16, tq.COMPUTE_FP32))
+
+    def best(cfg):
+        with tq.Plan(pat, cfg) as plan:
+            reps = [plan.reconstruct(r5["frame"]) for _ in range(4)][1:]
+        return min(reps, key=lambda r: r.seconds)
+
+    f16, f32 = (best(_protocol(tq, tq.ALGO_RLJSDE, w, tq.COMPUTE_FP32)) for w in (16, 32))
+    rl16, rl32 = (best(_protocol(tq, tq.ALGO_RLJSDE, w, tq.COMPUTE_FP64)) for w in (16, 32))
 
     def per_block(rep):
         return rep.seconds / rep.blocks_processed
 
     l_ratio = per_block(r0["l"]) / per_block(l16)
-    rl_ratio = per_block(r0["rl"]) / per_block(rl16)
-    f_ratio = per_block(r5["f32"]) / per_block(f16)
+    rl_ratio = per_block(rl32) / per_block(rl16)
+    f_ratio = per_block(f32) / per_block(f16)
     print(f"per-block W32/W16: ljsde {l_ratio:.2f}, rljsde fp64 {rl_ratio:.2f}, fp32 {f_ratio:.2f}")
     assert 8.0 <= l_ratio <= 32.0, l_ratio
     assert 2.0 <= f_ratio <= 8.0, f_ratio
