@@ -103,7 +103,8 @@ int validate(const tqsb_config& c, int period) {
 // window row per warp, or B > 16, beyond its 8 kept pixels per lane -- which the
 // reference accepts and the fp64 kernel runs on the reference's exact greedy paths)
 bool uses_f32(const tqsb_config& c) {
-    return c.compute == TQSB_COMPUTE_FP32 && c.window <= kMaxWindowF32 && c.block * c.block <= 256;
+    return c.algorithm == TQSB_ALGO_RLJSDE && c.compute == TQSB_COMPUTE_FP32 &&
+           c.window <= kMaxWindowF32 && c.block * c.block <= 256;
 }
 
 // the fp64 RL-JSDE kernel on Precision::Single planes, like the reference's float
@@ -529,6 +530,7 @@ int alloc_class(tqsb_plan* p, Device* d, const tqsb_config& c, int key, int orow
     tab.d64 = cb->d64;
     tab.cells = nullptr;
     tab.w64 = cb->w;
+    tab.bt64 = cb->t64;  // B transposed, written over the T scratch after the build
     tab.local = int(L);
     d->slot_of[key] = int(d->tabs.size());
     d->tabs.push_back(tab);
@@ -1196,7 +1198,7 @@ void fill_report(tqsb_report* rep, const std::vector<BandResult>& rs, const tqsb
     rep->psnr_db = 0.0;
     rep->has_psnr = 0;
     rep->gpu_launches = launches;
-    rep->compute = uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE ? TQSB_COMPUTE_FP32 : TQSB_COMPUTE_FP64;
+    rep->compute = uses_f32(c) ? TQSB_COMPUTE_FP32 : TQSB_COMPUTE_FP64;
 }
 
 // L-JSDE keeps no kernel cache in the reference (pipeline.cpp:111-112, 173-177):
@@ -1511,8 +1513,7 @@ int device_band(tqsb_plan* p, const tqsb_config* call, const double* d_frame, in
         rep->cache_misses = created;
         rep->cache_hits = w->n_tasks + (w->classes_total - created);
         rep->gpu_launches = launches;
-        rep->compute = uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE ? TQSB_COMPUTE_FP32
-                                                                        : TQSB_COMPUTE_FP64;
+        rep->compute = uses_f32(c) ? TQSB_COMPUTE_FP32 : TQSB_COMPUTE_FP64;
         ljsde_report(c, rep);
     }
     return TQSB_OK;
@@ -1829,7 +1830,13 @@ int tqsb_plan_load_tables(tqsb_plan* p, const char* path, int* classes_out) {
                                      cudaMemcpyHostToDevice, d->stream));
             CUDA_TRY(cudaMemcpyAsync(cb.d64, dv.data(), sizeof(double) * K, cudaMemcpyHostToDevice,
                                      d->stream));
-            // the planes are the cache; the fp32 product tables are derived on first use
+            // the planes are the cache; the fp32 product tables are derived on first use;
+            // the transposed B of the batched L-JSDE kernel is rebuilt from the loaded B
+            int launches = 0;
+            const int rc = launch_tables_transpose(&cb, 1, window, cb.local, d->stream, &launches);
+            if (rc != 0)
+                return set_error(TQSB_ECUDA, std::string("table transpose: ") +
+                                                 cudaGetErrorString(cudaError_t(rc)));
             CUDA_TRY(cudaStreamSynchronize(d->stream));  // b/c/dv are reused next record
         }
         ++installed;

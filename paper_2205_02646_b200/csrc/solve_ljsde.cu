@@ -18,9 +18,12 @@
 // ... (each summed over m in order, so the arithmetic per k is the reference's), the
 // first-max selection is a CTA reduction with ties to the smaller k, and the residual
 // (L <= K/4 complex) lives in shared memory. Synthesis and placement as in solve_f64.cu.
+// For W <= 32 the batched variant below (NB blocks of a class per CTA) is launched; this
+// per-block kernel serves larger windows and single-block tracing.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "tqsb_internal.hpp"
 
@@ -200,11 +203,297 @@ __global__ void __launch_bounds__(kThreadsL) k_solve_ljsde(const SolveArgs a, do
     }
 }
 
+// ---------------------------------------------------------------------------
+// Batched L-JSDE (W <= 32): NB blocks of one class per CTA, in lock step. Every
+// iteration each thread takes its frequencies k (tid, tid + 256, ...) and sums the
+// numerators of all NB blocks in one pass over m, reading the class's B in its
+// transposed, m-major copy (ClassTab::bt64: one coalesced 16 B load per thread per m,
+// shared by the NB blocks, instead of one strided B row per block). Per block and k
+// the sum still runs over m in ascending order with the same expression, and the
+// selection, step, residual update, energy stop, coefficient accumulation and
+// synthesis are the per-block kernel's, so the output is identical to it (and to the
+// reference's greedy paths). The residuals of the NB blocks live in shared memory; the
+// dense coefficients and first-touch order in a per-CTA global scratch.
+// ---------------------------------------------------------------------------
+struct BestN {
+    double s, nr, ni;
+    int k;
+};
+
+__device__ __forceinline__ BestN betterN(BestN a, BestN b) {
+    if (b.k < 0) return a;
+    if (a.k < 0) return b;
+    return (b.s > a.s || (b.s == a.s && b.k < a.k)) ? b : a;
+}
+
+template <int NB, int KT>
+__global__ void __launch_bounds__(kThreadsL, 2)
+    k_solve_ljsde_b(const SolveArgs a, int groups_per_item, double* coef_g, int* order_g,
+                    unsigned char* touched_g) {
+    extern __shared__ __align__(16) double2 smr[];  // [NB][L] residuals
+    __shared__ BestN s_best[kWarpsL][NB];
+    __shared__ int s_u[NB], s_done[NB], s_nact[NB], s_alive;
+    __shared__ double s_gr[NB], s_gi[NB];
+    const int W = a.window, K = W * W, B = a.block;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double2* coef = reinterpret_cast<double2*>(coef_g) + size_t(blockIdx.x) * NB * K;
+    int* order = order_g + size_t(blockIdx.x) * NB * K;
+    unsigned char* touched = touched_g + size_t(blockIdx.x) * NB * K;
+    const int n_groups = a.n_items * groups_per_item;
+    for (int gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+        const WorkItem item = a.items[gi / groups_per_item];
+        const int t0 = item.start + (gi % groups_per_item) * NB;
+        const int cnt = min(NB, item.start + item.count - t0);
+        if (cnt <= 0) continue;  // CTA-uniform
+        const ClassTab& ct = a.tabs[item.cls];
+        const int L = ct.local;
+        const double2* bt = reinterpret_cast<const double2*>(ct.bt64);
+        // r = y^local per block (gather_local_values, grid.cpp:104-114)
+        for (int idx = tid; idx < NB * L; idx += kThreadsL) {
+            const int b = idx / L, m = idx % L;
+            double v = 0.0;
+            if (b < cnt) {
+                const Task tk = a.tasks[t0 + b];
+                const int r0 = (tk.origin_row + 1) / 2;
+                const int c0 = (tk.origin_col + 1) / 2, c1 = (tk.origin_col + W - 2) / 2;
+                const int ncol = c1 - c0 + 1;
+                int fr = r0 + m / ncol, fc = c0 + m % ncol;
+                fr = fr < a.frame_rows - 1 ? fr : a.frame_rows - 1;
+                fc = fc < a.frame_cols - 1 ? fc : a.frame_cols - 1;
+                v = a.frame[size_t(fr - a.frame_row0) * a.frame_pitch + fc];
+            }
+            smr[idx] = make_double2(v, 0.0);
+        }
+        for (int idx = tid; idx < NB * K; idx += kThreadsL) {
+            coef[idx] = make_double2(0.0, 0.0);
+            touched[idx] = 0;
+        }
+        if (tid < NB) {
+            s_done[tid] = tid >= cnt;
+            s_nact[tid] = 0;
+        }
+        __syncthreads();
+        const double floor = a.early_stop ? a.early_stop_scale * L : -1.0;
+        for (int it = 0; it < a.iterations; ++it) {
+            unsigned live = 0;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) live |= s_done[b] ? 0u : 1u << b;
+            if (!live) break;  // CTA-uniform
+            BestN best[NB];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) best[b] = BestN{0.0, 0.0, 0.0, -1};
+            // KT frequencies per thread at once (k0 + 256 t), so each residual value read
+            // from shared memory feeds KT x 4 multiply-adds; k ascending per thread
+            for (int k0 = tid; k0 < K; k0 += kThreadsL * KT) {
+                double nr[KT][NB], ni[KT][NB];
+#pragma unroll
+                for (int t = 0; t < KT; ++t)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) nr[t][b] = ni[t][b] = 0.0;
+                const double2* col[KT];
+#pragma unroll
+                for (int t = 0; t < KT; ++t) {
+                    const int k = k0 + kThreadsL * t;
+                    col[t] = bt + (k < K ? k : 0);
+                }
+                // PF rows of B in flight (L2 hits of ~250+ cycles), sums in m order
+                constexpr int PF = 2;
+                int m = 0;
+                for (; m + PF <= L; m += PF) {
+                    double2 bb[PF][KT];
+#pragma unroll
+                    for (int j = 0; j < PF; ++j)
+#pragma unroll
+                        for (int t = 0; t < KT; ++t) bb[j][t] = __ldg(col[t] + size_t(m + j) * K);
+#pragma unroll
+                    for (int j = 0; j < PF; ++j) {
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            const double2 r = smr[b * L + m + j];
+#pragma unroll
+                            for (int t = 0; t < KT; ++t) {
+                                const double br = bb[j][t].x, bi = bb[j][t].y;
+                                nr[t][b] += br * r.x - bi * r.y;
+                                ni[t][b] += br * r.y + bi * r.x;
+                            }
+                        }
+                    }
+                }
+                for (; m < L; ++m) {
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const double2 r = smr[b * L + m];
+#pragma unroll
+                        for (int t = 0; t < KT; ++t) {
+                            const double2 bb = __ldg(col[t] + size_t(m) * K);
+                            nr[t][b] += bb.x * r.x - bb.y * r.y;
+                            ni[t][b] += bb.x * r.y + bb.y * r.x;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < KT; ++t) {
+                    const int k = k0 + kThreadsL * t;
+                    if (k >= K) break;
+                    const double den = ct.d64[k];
+                    if (den <= 0.0) continue;
+                    const double q = a.wc.q64[k];
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        if (!(live >> b & 1u)) continue;
+                        const double s = q * (nr[t][b] * nr[t][b] + ni[t][b] * ni[t][b]) / den;
+                        if (best[b].k < 0 || s > best[b].s) best[b] = BestN{s, nr[t][b], ni[t][b], k};
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    BestN o;
+                    o.s = __shfl_xor_sync(FULL, best[b].s, off);
+                    o.nr = __shfl_xor_sync(FULL, best[b].nr, off);
+                    o.ni = __shfl_xor_sync(FULL, best[b].ni, off);
+                    o.k = __shfl_xor_sync(FULL, best[b].k, off);
+                    best[b] = betterN(best[b], o);
+                }
+                if (lane == 0) s_best[warp][b] = best[b];
+            }
+            __syncthreads();
+            if (tid < NB && (live >> tid & 1u)) {
+                const int b = tid;
+                BestN bb = s_best[0][b];
+                for (int w = 1; w < kWarpsL; ++w) bb = betterN(bb, s_best[w][b]);
+                if (bb.k < 0) {  // no admissible frequency: this block stops (ljsde.cpp:150)
+                    s_done[b] = 1;
+                    s_u[b] = -1;
+                } else {
+                    const int u = bb.k;
+                    const double den = ct.d64[u];
+                    const double gr = a.step * (bb.nr / den), gi = a.step * (bb.ni / den);
+                    double2& c = coef[size_t(b) * K + u];
+                    c.x += gr;
+                    c.y += gi;
+                    if (!touched[size_t(b) * K + u]) {
+                        touched[size_t(b) * K + u] = 1;
+                        order[size_t(b) * K + s_nact[b]++] = u;
+                    }
+                    s_u[b] = u;
+                    s_gr[b] = gr;
+                    s_gi[b] = gi;
+                }
+            } else if (tid < NB) {
+                s_u[tid] = -1;
+            }
+            __syncthreads();
+            // r_m -= g conj(T_mu), T from the stored w T (ljsde.cpp:163-170)
+            for (int idx = tid; idx < cnt * L; idx += kThreadsL) {
+                const int b = idx / L, m = idx % L;
+                const int u = s_u[b];
+                if (u < 0) continue;
+                const double* col = ct.b64 + size_t(u) * L * 2;
+                const double gr = s_gr[b], gi = s_gi[b];
+                const double wm = ct.w64[m];
+                const double tr = col[2 * m] / wm, tim = -col[2 * m + 1] / wm;
+                double2 r = smr[idx];
+                r.x -= gr * tr - gi * tim;
+                r.y -= gr * tim + gi * tr;
+                smr[idx] = r;
+            }
+            __syncthreads();
+            if (a.early_stop) {  // energy stop, summed in m order like the reference
+                if (tid < cnt && s_u[tid] >= 0) {
+                    double es = 0.0;
+                    for (int m = 0; m < L; ++m) {
+                        const double2 r = smr[tid * L + m];
+                        es += (r.x * r.x + r.y * r.y) * ct.w64[m];
+                    }
+                    if (es < floor) s_done[tid] = 1;
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+        // synthesize_real (basis.cpp:52-73) over the kept pixels, then place
+        for (int p = tid; p < cnt * B * B; p += kThreadsL) {
+            const int b = p / (B * B), q = p % (B * B);
+            const Task tk = a.tasks[t0 + b];
+            const int rw = tk.block_row - tk.origin_row, cw = tk.block_col - tk.origin_col;
+            const int eta = rw + q / B, gam = cw + q % B;
+            double v = 0.0;
+            const int na = s_nact[b];
+            for (int t = 0; t < na; ++t) {
+                const int f = order[size_t(b) * K + t];
+                const int idx = (eta * (f / W) + gam * (f % W)) % W;
+                const double2 c = coef[size_t(b) * K + f];
+                v += c.x * a.wc.unit64[2 * idx] - c.y * a.wc.unit64[2 * idx + 1];
+            }
+            const int orow = tk.block_row + q / B, ocol = tk.block_col + q % B;
+            if (orow < a.out_rows && ocol < a.out_cols) {
+                if (a.clip) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+                a.out[size_t(orow - a.out_row0) * a.out_cols + ocol] = v;
+            }
+        }
+        __syncthreads();  // the next group reuses the shared residuals and the scratch
+    }
+}
+
+template <int NB, int KT>
+int launch_batched(const SolveArgs& a, cudaStream_t st, int num_sms, int max_item) {
+    const int K = a.window * a.window;
+    const size_t smem = size_t(NB) * (K / 4 + 1) * sizeof(double2);
+    cudaError_t e = cudaFuncSetAttribute(k_solve_ljsde_b<NB, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    const int gpi = (max_item + NB - 1) / NB;
+    const int groups = a.n_items * gpi;
+    int grid = 2 * num_sms;
+    grid = groups < grid ? groups : grid;
+    if (grid < 1) grid = 1;
+    const size_t per = size_t(NB) * K;
+    char* scratch = nullptr;
+    e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), size_t(grid) * per * (16 + 4 + 1), st);
+    if (e != cudaSuccess) return e;
+    double* coef = reinterpret_cast<double*>(scratch);
+    int* order = reinterpret_cast<int*>(scratch + size_t(grid) * per * 16);
+    unsigned char* touched = reinterpret_cast<unsigned char*>(scratch + size_t(grid) * per * 20);
+    k_solve_ljsde_b<NB, KT><<<grid, kThreadsL, smem, st>>>(a, gpi, coef, order, touched);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaFreeAsync(scratch, st);
+}
+
 }  // namespace
 
 int launch_solve_ljsde(const SolveArgs& a, void* stream, int num_sms) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int K = a.window * a.window;
+    // the batched kernel for W <= 32 (L <= K / 4 residuals per block in shared memory,
+    // the m-major B copy present); tracing and the forced global-state test path keep
+    // the per-block kernel
+    if (a.window <= 32 && !a.trace_picks && !force_global_state() && a.items && a.n_items > 0) {
+        // tasks per work item (plan.cpp prepare_band: 4 x the warps of the kernel family);
+        // the largest family bounds it, so no task of an item is left out
+        const int max_item = 4 * (kWarpsF32 > kWarpsF64 ? kWarpsF32 : kWarpsF64);
+        // enough groups to fill two CTAs per SM: 8 blocks per CTA when the frame allows
+        const int n_tasks = a.n_tasks;
+        const char* nbv = std::getenv("TQSB_LJSDE_NB");  // experiment override
+        // measured at 512^2 / P = 32 (tools/ljsde_bench.py): 2 blocks x 4 frequencies per
+        // thread 0.57 s, 4 x 2 0.94 s, 1 x 4 0.75 s -- two blocks once the frame fills the
+        // GPU with two CTAs per SM, else one
+        const int nb = nbv ? std::atoi(nbv) : n_tasks >= 2 * 2 * num_sms ? 2 : 1;
+        // frequencies per thread: K / 256 rounded up (no lanes on k >= K)
+        const int kt = K > 512 ? 4 : K > 256 ? 2 : 1;
+        if (nb == 4) return launch_batched<4, 2>(a, st, num_sms, max_item);
+        if (nb == 2) {
+            if (kt == 4) return launch_batched<2, 4>(a, st, num_sms, max_item);
+            if (kt == 2) return launch_batched<2, 2>(a, st, num_sms, max_item);
+            return launch_batched<2, 1>(a, st, num_sms, max_item);
+        }
+        if (kt == 4) return launch_batched<1, 4>(a, st, num_sms, max_item);
+        if (kt == 2) return launch_batched<1, 2>(a, st, num_sms, max_item);
+        return launch_batched<1, 1>(a, st, num_sms, max_item);
+    }
     const size_t smem = ljsde_state_doubles(K) * sizeof(double);
     if (smem > 227 * 1024 || force_global_state()) {  // W >= 74: state in global memory, one CTA per SM
         double* scratch = nullptr;

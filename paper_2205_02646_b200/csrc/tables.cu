@@ -202,6 +202,26 @@ __global__ void k_pack32(const ClassBuild* __restrict__ cls, int W, int k_pad,
     reinterpret_cast<float4*>(c.cpack)[size_t(ur) * (k_pad / 2) + pair] = v;
 }
 
+// bt[m*K + k] = b[k*L + m] (complex), into the T scratch once the Gram kernel is done
+// with it: 32x32 tiles through shared memory, coalesced both ways
+__global__ void k_transpose_b(const ClassBuild* __restrict__ cls, int W) {
+    const ClassBuild c = cls[blockIdx.z];
+    const int K = W * W, L = c.local;
+    __shared__ double2 tile[32][33];
+    const int k0 = blockIdx.y * 32, m0 = blockIdx.x * 32;
+    const double2* b = reinterpret_cast<const double2*>(c.b64);
+    double2* bt = reinterpret_cast<double2*>(c.t64);
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int k = k0 + i, m = m0 + threadIdx.x;
+        if (k < K && m < L) tile[i][threadIdx.x] = b[size_t(k) * L + m];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int m = m0 + i, k = k0 + threadIdx.x;
+        if (k < K && m < L) bt[size_t(m) * K + k] = tile[threadIdx.x][i];
+    }
+}
+
 // The reference's Precision::Single planes (fill_planes<float>, rljsde.cpp:70-100): B, C
 // and D stored as float from the double accumulations, widened to double in the loop
 // (KernelPlanes::dAt and the update's casts) -- here rounded in place in the fp64 planes.
@@ -253,6 +273,31 @@ int launch_tables_build(const void* host_descs, int n, int window, const double*
             k_round_single<<<g, 256, 0, stream>>>(d, window);
             if (launches) *launches += 1;
         }
+        {
+            dim3 g((max_local + 31) / 32, (K + 31) / 32, nz);
+            k_transpose_b<<<g, dim3(32, 8), 0, stream>>>(d, window);
+            if (launches) *launches += 1;
+        }
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaFreeAsync(dd, stream);
+}
+
+int launch_tables_transpose(const void* host_descs, int n, int window, int max_local, void* stream_,
+                            int* launches) {
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    ClassBuild* dd = nullptr;
+    cudaError_t e = cudaMallocAsync(&dd, sizeof(ClassBuild) * n, stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(dd, host_descs, sizeof(ClassBuild) * n, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return e;
+    const int K = window * window;
+    for (int z0 = 0; z0 < n; z0 += 65535) {
+        const int nz = n - z0 < 65535 ? n - z0 : 65535;
+        dim3 g((max_local + 31) / 32, (K + 31) / 32, nz);
+        k_transpose_b<<<g, dim3(32, 8), 0, stream>>>(dd + z0, window);
+        if (launches) *launches += 1;
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

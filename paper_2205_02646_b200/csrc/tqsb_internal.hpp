@@ -47,6 +47,8 @@ struct ClassTab {
     const double* d64;    // K
     const int* cells;     // L x (cell frame row offset, cell frame col offset) vs window origin
     const double* w64;    // L spatial weights (basis.cpp:75-88; L-JSDE residual update)
+    const double* bt64;   // L*K complex interleaved, m-major [m*K+k]: B transposed for the
+                          // batched L-JSDE kernel (stored in the build's T scratch)
     int local;            // L
     int pad;
 };
@@ -139,6 +141,10 @@ struct ClassBuild {
 // to float (the reference's Precision::Single).
 int launch_tables_build(const void* host_descs, int n, int window, const double* unit64,
                         int max_local, void* stream, int* launches, int round_single);
+// B transposed to m-major into the (then dead) T scratch of n classes (the batched L-JSDE
+// kernel's coalesced layout); part of launch_tables_build, separately after a TQSK load
+int launch_tables_transpose(const void* host_descs, int n, int window, int max_local, void* stream,
+                            int* launches);
 // fp32 product tables (scale, fac, cpack) of n classes from their resident fp64
 // planes, for one (q = frequency weights, step width gamma).
 int launch_tables_derive(const void* host_descs, int n, int window, int k_pad, double step,

@@ -82,9 +82,7 @@ def test_criterion5_recurrent_speedup(need_gpu, runs):
 
 
 def test_criterion6_window_scaling(tq, need_gpu, runs):
-    r0 = runs[0]
     pat = tq.generate_pattern(7, 32)
-    l16 = _run(tq, pat, r0["frame"], _protocol(tq, tq.ALGO_LJSDE, 16))
     # the RL-JSDE kernels on the 512^2 image: 1,024 blocks leave the B200's warps mostly
     # idle and the few-ms launches are dominated by fixed costs (the fp64 ratio on 128^2
     # ranged 1.6-7.3 run to run); per-block time = the best of three calls
@@ -96,12 +94,13 @@ def test_criterion6_window_scaling(tq, need_gpu, runs):
         return min(reps, key=lambda r: r.seconds)
 
     f16, f32 = (best(_protocol(tq, tq.ALGO_RLJSDE, w, tq.COMPUTE_FP32)) for w in (16, 32))
+    l16, l32 = (best(_protocol(tq, tq.ALGO_LJSDE, w)) for w in (16, 32))
     rl16, rl32 = (best(_protocol(tq, tq.ALGO_RLJSDE, w, tq.COMPUTE_FP64)) for w in (16, 32))
 
     def per_block(rep):
         return rep.seconds / rep.blocks_processed
 
-    l_ratio = per_block(r0["l"]) / per_block(l16)
+    l_ratio = per_block(l32) / per_block(l16)
     rl_ratio = per_block(rl32) / per_block(rl16)
     f_ratio = per_block(f32) / per_block(f16)
     print(f"per-block W32/W16: ljsde {l_ratio:.2f}, rljsde fp64 {rl_ratio:.2f}, fp32 {f_ratio:.2f}")

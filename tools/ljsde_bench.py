@@ -33,7 +33,7 @@ res = {"image": [a.rows, a.rows], "window": a.window, "iterations": a.iterations
 want_l = None
 for algo in (() if a.no_reference else ("ljsde", "rljsde")):
     t = time.perf_counter()
-    want, sec = ref.reconstruct_algo(frame, pat.opaque, 8, algo, window=a.window,
+    want, sec = ref.reconstruct_algo(frame, pat.opaque, a.period, algo, window=a.window,
                                      iterations=a.iterations, threads=0)
     res[f"reference_{algo}_s"] = sec
     res[f"reference_{algo}_wall_s"] = time.perf_counter() - t
