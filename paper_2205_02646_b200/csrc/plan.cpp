@@ -312,7 +312,6 @@ struct Work {
     // within a chunk); chunk s holds chunk_count[s] blocks covering block rows
     // [chunk_br[s], chunk_br[s+1])
     std::vector<int> chunk_count, chunk_br;
-    std::vector<int> chunk_fr_hi;  // frame rows [frame_row0, chunk_fr_hi[s]) cover chunk s
 };
 constexpr int kStreamChunks = 16;       // output chunks of a streamed host-buffer call
 constexpr int kStreamMinTasks = 8192;   // below this a frame is not worth streaming
@@ -349,8 +348,7 @@ struct Device {
     float* d_unit32 = nullptr;
     double* d_unit64 = nullptr;
     uint8_t* d_opaque = nullptr;   // the pattern's (P/2)^2 quadrant indices (device readout)
-    int* d_progress = nullptr;     // chunk counters of a streamed call (device memory):
-                                   // [0, 64) blocks finished, [64, 128) input rows ready
+    int* d_progress = nullptr;     // blocks finished per chunk of a streamed call (device)
     cudaEvent_t ev_chunk[64] = {}; // chunk s copied to the pinned staging
     int* d_counters = nullptr;     // kCounterRing dynamic task-queue heads
     unsigned counter_next = 0;
@@ -466,8 +464,8 @@ void device_free(Device* d) {
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // memcpy of large host buffers (pageable <-> pinned staging) on up to max_threads threads
-void par_memcpy(void* dst, const void* src, size_t bytes, unsigned max_threads = 8) {
-    const size_t kPerThread = size_t(2) << 20;  // at least 2 MB per thread
+void par_memcpy(void* dst, const void* src, size_t bytes, unsigned max_threads = 16) {
+    const size_t kPerThread = size_t(1) << 20;  // at least 1 MB per thread
     unsigned nt = std::min<unsigned>(max_threads, std::max(1u, std::thread::hardware_concurrency()));
     nt = unsigned(std::min<size_t>(nt, bytes / kPerThread));
     if (nt <= 1) {
@@ -701,7 +699,6 @@ int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& 
         w.chunk_br.push_back(s == n_chunks ? br1 : b);
     }
     w.chunk_count.assign(n_chunks, 0);
-    w.chunk_fr_hi.assign(n_chunks, w.frame_row0);
     std::vector<Task> sorted;
     std::vector<WorkItem> items;
     std::vector<int> task_cls;
@@ -711,12 +708,7 @@ int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& 
         std::vector<std::vector<Task>> by_key(size_t(p->period) * p->period);
         for (size_t i = 0; i < e.tasks.size(); ++i) {
             const int bri = e.tasks[i].block_row / g.B;
-            if (bri >= w.chunk_br[ch] && bri < w.chunk_br[ch + 1]) {
-                by_key[e.keys[i]].push_back(e.tasks[i]);
-                // frame rows this chunk's windows read: through (origin + W - 1) / 2
-                w.chunk_fr_hi[ch] = std::max(w.chunk_fr_hi[ch],
-                                             std::min(frame_rows, (e.tasks[i].origin_row + g.W - 1) / 2 + 1));
-            }
+            if (bri >= w.chunk_br[ch] && bri < w.chunk_br[ch + 1]) by_key[e.keys[i]].push_back(e.tasks[i]);
         }
         for (int k : e.class_order) {
             const auto& v = by_key[k];
@@ -875,21 +867,6 @@ WaitValue32Fn wait_value32() {
     return fn;
 }
 
-using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-WriteValue32Fn write_value32() {
-    static WriteValue32Fn fn = [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess) {
-            cudaGetLastError();
-            return WriteValue32Fn(nullptr);
-        }
-        return reinterpret_cast<WriteValue32Fn>(f);
-    }();
-    return fn;
-}
-
 // Host-buffer band run on device d: H2D of the band's frame rows (halo included),
 // one solve launch whose B x B output tiles are stored straight into pinned host
 // memory (zero-copy: the caller's buffer when it is pinned, else the plan's pinned
@@ -914,7 +891,7 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
                                c.hot_columns <= 0 &&
                                solve_f32_streams(p->wt.NS, c.block * c.block) &&
                                n_est >= kStreamMinTasks && br1 - br0 >= kStreamChunks &&
-                               wait_value32() != nullptr && write_value32() != nullptr
+                               wait_value32() != nullptr
                            ? kStreamChunks
                            : 0;
     Work* w = nullptr;
@@ -939,15 +916,16 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
     if (stream) {
         if ((rc = ensure_buffer(&d->d_out, &d->out_cap, out_n))) return fail(rc);
         if (!d->d_progress) {
-            CUDA_TRY_V(cudaMalloc(&d->d_progress, sizeof(int) * 128));
+            CUDA_TRY_V(cudaMalloc(&d->d_progress, sizeof(int) * 64));
             for (auto& e : d->ev_chunk) CUDA_TRY_V(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
     }
     const double* src = frame + size_t(fr0) * frame_cols;
-    // a streamed call with a pageable frame stages its rows chunk by chunk after the
-    // launch; the kernel waits per chunk on an input-ready flag (SolveArgs::in_ready)
-    const bool stream_in = stream && !in_pinned;
-    if (!in_pinned && !stream_in) {
+    // The input is staged before the launch: a kernel that waited on rows staged after
+    // its launch (an input-ready flag per chunk) would deadlock wherever launches are
+    // synchronous -- CUDA_LAUNCH_BLOCKING=1, compute-sanitizer, ncu -- so the streamed
+    // call streams its output only and the kernel never waits on later stream work.
+    if (!in_pinned) {
         par_memcpy(d->h_in, src, sizeof(double) * in_n);
         src = d->h_in;
     }
@@ -959,8 +937,7 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
         cudaGetLastError();
         return fail(set_error(TQSB_ECUDA, "output buffer is not device-mapped pinned memory"));
     }
-    if (!stream_in)
-        cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
+    cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
     SolveArgs a = base_args(p, d, c, dv);
     a.frame = d->d_frame;
     a.frame_rows = frame_rows;
@@ -984,11 +961,9 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
     };
     if (stream) {
         a.progress = d->d_progress;
-        a.in_ready = stream_in ? d->d_progress + 64 : nullptr;
-        CUDA_TRY_V(cudaMemsetAsync(d->d_progress, 0, sizeof(int) * 128, d->stream));
+        CUDA_TRY_V(cudaMemsetAsync(d->d_progress, 0, sizeof(int) * stream, d->stream));
         CUDA_TRY_V(cudaEventRecord(d->ev_h2d[2], d->stream));  // counters zeroed
         CUDA_TRY_V(cudaStreamWaitEvent(d->s_d2h, d->ev_h2d[2], 0));
-        CUDA_TRY_V(cudaStreamWaitEvent(d->s_h2d, d->ev_h2d[2], 0));
     }
     cudaEventRecord(d->ev0, d->stream);
     if (w->n_items > 0) {
@@ -996,36 +971,6 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
         r->launches += 1;
     }
     cudaEventRecord(d->ev1, d->stream);
-    if (stream_in) {  // frame rows chunk by chunk: stage, copy, raise the chunk's flag
-        WriteValue32Fn writev = write_value32();
-        int done = fr0;
-        for (int s = 0; s < stream; ++s) {
-            // whole 128 B lines: a line the kernel reads for chunk s never holds rows
-            // that are not on the device yet
-            size_t b0 = size_t(done - fr0) * frame_cols * sizeof(double);
-            size_t b1 = size_t(std::max(done, w->chunk_fr_hi[s]) - fr0) * frame_cols * sizeof(double);
-            b1 = std::min(in_n * sizeof(double), (b1 + 127) / 128 * 128);
-            b0 = std::min(b0, b1);
-            if (b1 > b0) {
-                par_memcpy(reinterpret_cast<char*>(d->h_in) + b0, reinterpret_cast<const char*>(src) + b0,
-                           b1 - b0, 4);
-                cudaMemcpyAsync(reinterpret_cast<char*>(d->d_frame) + b0,
-                                reinterpret_cast<const char*>(d->h_in) + b0, b1 - b0,
-                                cudaMemcpyHostToDevice, d->s_h2d);
-            }
-            done = std::max(done, fr0 + int(b1 / (sizeof(double) * frame_cols)));
-            if (writev(reinterpret_cast<CUstream>(d->s_h2d),
-                       reinterpret_cast<CUdeviceptr>(d->d_progress + 64 + s), 1,
-                       CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
-                // release the waiting kernel before failing (it must not spin forever)
-                std::vector<int> one(stream, 1);
-                cudaStreamSynchronize(d->s_h2d);
-                cudaMemcpy(d->d_progress + 64, one.data(), sizeof(int) * stream, cudaMemcpyHostToDevice);
-                cudaStreamSynchronize(d->stream);
-                return fail(set_error(TQSB_ECUDA, "cuStreamWriteValue32 failed"));
-            }
-        }
-    }
     std::thread prefault;  // joined before returning (the buffer is the caller's)
     struct Joiner {
         std::thread& t;

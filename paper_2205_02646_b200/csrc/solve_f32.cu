@@ -68,7 +68,7 @@ struct Scratch {
 // NW warps per CTA (1 CTA per SM): 16 at 128 registers where the kernel fits without
 // spilling in the loop (the default W = 32 / B = 4 product path: 38.8 vs 40.5 ms per 4K frame at 12),
 // 12 at 168 registers for the heavier instantiations (B >= 8, TMEM tier, tracing)
-// SP: the streamed host-buffer variant (SolveArgs::progress / in_ready, chunk-tagged
+// SP: the streamed host-buffer variant (SolveArgs::progress, chunk-tagged
 // task list); a separate instantiation so the device-resident path carries none of it
 template <int NS, int W, int PPL, bool TRACE, bool TM, int NW, bool SP = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
@@ -366,25 +366,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         // warp-level dynamic scheduling over the class-sorted task list: no CTA-wide
         // class state (per-rank factors are read through L1), and no tail imbalance
         // beyond one block per warp
-        int ready = -1;  // streamed input: chunks known to be on the device
         for (;;) {
             int ti = 0;
             if (lane == 0) ti = atomicAdd(a.counter, 1);
             ti = __shfl_sync(FULL, ti, 0);
             if (ti >= a.n_tasks) break;
             const int tc = __ldg(a.task_cls + ti);
-            if (SP && a.in_ready && (tc >> kTaskClsBits) > ready) {
-                // chunks are handed out in order: wait for this one's frame rows once
-                // (the frame reads below depend on the flag through this branch, and no
-                // line of these rows was read before they landed)
-                const int ch = tc >> kTaskClsBits;
-                if (lane == 0) {
-                    volatile const int* f = a.in_ready + ch;
-                    while (*f == 0) __nanosleep(256);
-                }
-                __syncwarp();
-                ready = ch;
-            }
             if constexpr (SP)
                 solve_task(ti, a.tabs[tc & ((1 << kTaskClsBits) - 1)], tc >> kTaskClsBits);
             else

@@ -98,10 +98,6 @@ struct SolveArgs {
     // stores), which a copy stream waits on (cuStreamWaitValue32) to move finished
     // output rows to the host while the kernel runs
     int* progress;
-    // streamed input: when non-null, the frame rows of chunk s are on the device once
-    // in_ready[s] != 0 (written by the copy stream after their H2D); a warp checks the
-    // flag before its first task of each chunk
-    int* in_ready;
 };
 constexpr int kTaskClsBits = 20;  // task_cls = class slot | chunk << kTaskClsBits
 // the fp32 kernel has a streamed instantiation for NS == 16 slots (W = 23..32) and

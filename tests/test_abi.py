@@ -148,3 +148,44 @@ def test_output_buffers_are_validated():
     ro.flags.writeable = False
     with pytest.raises(ValueError):
         tq._out_array(ro, (4, 6))
+
+
+def test_per_call_entry_points_reject_null_arguments(tq):
+    """The *_with entry points (per-call config over a shared plan) fail cleanly on a
+    null plan or buffer, with EINVAL (std::invalid_argument) -- no device needed."""
+    import ctypes as C
+    cfg = tq.ReconstructionConfig()._c()
+    buf = np.zeros(16)
+    rep = tq._Report()
+    for rc in (tq.lib.tqsb_reconstruct_with(None, C.byref(cfg), tq._d(buf), 2, 2, tq._d(buf), None,
+                                            C.byref(rep)),
+               tq.lib.tqsb_reconstruct_band_with(None, C.byref(cfg), tq._d(buf), 2, 2, 0, 1,
+                                                 tq._d(buf), C.byref(rep)),
+               tq.lib.tqsb_reconstruct_batch_with(None, C.byref(cfg), None, 1, 2, 2, None,
+                                                  C.byref(rep)),
+               tq.lib.tqsb_reconstruct_device_with(None, C.byref(cfg), None, 2, 2, None, None,
+                                                   C.byref(rep))):
+        assert rc == tq.TQSB_EINVAL
+    assert "null" in tq.lib.tqsb_last_error().decode()
+
+
+def test_report_struct_matches_header(tq):
+    """tqsb_report gained `compute` (the arithmetic a call ran in): the ctypes mirror and
+    the header agree on the field order."""
+    import os
+    import re as _re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "include", "tqsb", "tqsb.h")).read()
+    body = hdr[hdr.index("typedef struct tqsb_report {"):hdr.index("} tqsb_report;")]
+    fields = _re.findall(r"^\s+(?:double|long long|int)\s+(\w+);", body, _re.M)
+    assert fields == [f for f, _ in tq._Report._fields_]
+
+
+def test_config_struct_matches_header(tq):
+    import os
+    import re as _re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "include", "tqsb", "tqsb.h")).read()
+    body = hdr[hdr.index("typedef struct tqsb_config {"):hdr.index("} tqsb_config;")]
+    fields = _re.findall(r"^\s+(?:double|int)\s+(\w+);", body, _re.M)
+    assert fields == [f for f, _ in tq._Config._fields_]
