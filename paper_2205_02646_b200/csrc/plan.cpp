@@ -312,8 +312,9 @@ struct Work {
     // within a chunk); chunk s holds chunk_count[s] blocks covering block rows
     // [chunk_br[s], chunk_br[s+1])
     std::vector<int> chunk_count, chunk_br;
+    std::vector<int> chunk_fr_hi;  // frame rows [frame_row0, chunk_fr_hi[s]) cover chunk s
 };
-constexpr int kStreamChunks = 16;       // output chunks of a streamed host-buffer call
+constexpr int kStreamChunks = 16;       // output chunks of a streamed host-buffer call (max)
 constexpr int kStreamMinTasks = 8192;   // below this a frame is not worth streaming
 
 // The per-call derived tables of one option set. The cache proper is the fp64 planes
@@ -699,6 +700,7 @@ int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& 
         w.chunk_br.push_back(s == n_chunks ? br1 : b);
     }
     w.chunk_count.assign(n_chunks, 0);
+    w.chunk_fr_hi.assign(n_chunks, w.frame_row0);
     std::vector<Task> sorted;
     std::vector<WorkItem> items;
     std::vector<int> task_cls;
@@ -708,7 +710,12 @@ int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& 
         std::vector<std::vector<Task>> by_key(size_t(p->period) * p->period);
         for (size_t i = 0; i < e.tasks.size(); ++i) {
             const int bri = e.tasks[i].block_row / g.B;
-            if (bri >= w.chunk_br[ch] && bri < w.chunk_br[ch + 1]) by_key[e.keys[i]].push_back(e.tasks[i]);
+            if (bri >= w.chunk_br[ch] && bri < w.chunk_br[ch + 1]) {
+                by_key[e.keys[i]].push_back(e.tasks[i]);
+                // frame rows the chunk's windows read: through (origin + W - 1) / 2
+                w.chunk_fr_hi[ch] = std::max(
+                    w.chunk_fr_hi[ch], std::min(frame_rows, (e.tasks[i].origin_row + g.W - 1) / 2 + 1));
+            }
         }
         for (int k : e.class_order) {
             const auto& v = by_key[k];
@@ -886,13 +893,18 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
     // host hands them to the caller's buffer -- so the staging copy and the first-touch
     // page faults of a fresh buffer overlap the solve instead of following it.
     const long long n_est = (long long)(br1 - br0) * (g.padN / g.B);
+    // Chunk-major order interleaves the classes: every chunk sweeps all of them, which is
+    // free while their C' tables share the L2 (P = 8: 4 interior classes, 32 MB) and costs
+    // HBM re-reads when they do not (P = 32: 64 classes, 512 MB) -- fewer chunks then.
+    const int per_axis = p->period / std::gcd(p->period, c.block);
+    const int n_chunks = std::clamp(128 / std::max(1, per_axis * per_axis), 1, kStreamChunks);
     // (the warp-scheduled kernel only: the TMEM column tier runs CTA work items)
-    const int stream = !out_pinned && uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE &&
+    const int stream = uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE &&
                                c.hot_columns <= 0 &&
                                solve_f32_streams(p->wt.NS, c.block * c.block) &&
                                n_est >= kStreamMinTasks && br1 - br0 >= kStreamChunks &&
-                               wait_value32() != nullptr
-                           ? kStreamChunks
+                               n_chunks >= 2 && wait_value32() != nullptr
+                           ? n_chunks
                            : 0;
     Work* w = nullptr;
     Derived* dv = nullptr;
@@ -909,9 +921,7 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
     const size_t in_n = size_t(fr1 - fr0) * frame_cols;
     const int orow0 = br0 * g.B, orow1 = std::min(br1 * g.B, g.M);
     const size_t out_n = size_t(std::max(0, orow1 - orow0)) * g.N;
-    const bool in_pinned = is_pinned(frame);
     if ((rc = ensure_buffer(&d->d_frame, &d->frame_cap, in_n))) return fail(rc);
-    if (!in_pinned && (rc = ensure_pinned(&d->h_in, &d->h_in_cap, in_n))) return fail(rc);
     if (!out_pinned && (rc = ensure_pinned(&d->h_out, &d->h_out_cap, out_n))) return fail(rc);
     if (stream) {
         if ((rc = ensure_buffer(&d->d_out, &d->out_cap, out_n))) return fail(rc);
@@ -921,14 +931,13 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
         }
     }
     const double* src = frame + size_t(fr0) * frame_cols;
-    // The input is staged before the launch: a kernel that waited on rows staged after
-    // its launch (an input-ready flag per chunk) would deadlock wherever launches are
-    // synchronous -- CUDA_LAUNCH_BLOCKING=1, compute-sanitizer, ncu -- so the streamed
-    // call streams its output only and the kernel never waits on later stream work.
-    if (!in_pinned) {
-        par_memcpy(d->h_in, src, sizeof(double) * in_n);
-        src = d->h_in;
-    }
+    // The input goes in one asynchronous copy before the launch; a pageable frame is staged
+    // by the driver, which pipelines its bounce buffers with the DMA (measured at 4K: +0.9
+    // to 1.3 ms over a pinned frame, against +1.2 / 1.6 / 2.6 ms for our own staging copy
+    // on 4 / 8 / 16 threads and +2.7 ms for cudaHostRegister + unregister per call). A
+    // kernel waiting on rows staged after its launch was faster still but would deadlock
+    // wherever launches are synchronous (CUDA_LAUNCH_BLOCKING=1, compute-sanitizer, ncu),
+    // so the kernel never waits on later stream work.
     double* host_out = out_pinned ? out_band : d->h_out;
     double* dev_view = nullptr;  // the pinned output as seen from the device (UVA)
     if (stream) {
@@ -937,7 +946,20 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
         cudaGetLastError();
         return fail(set_error(TQSB_ECUDA, "output buffer is not device-mapped pinned memory"));
     }
-    cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_n, cudaMemcpyHostToDevice, d->stream);
+    // A streamed call with a pageable frame runs as two launches: the first chunk (the
+    // largest, ~1/8 of the rows at 16 chunks) starts once its frame rows are copied, and
+    // the remaining rows are copied (the driver's host-side staging included) while it
+    // runs; the second launch waits for them through an event. Only stream order is
+    // involved -- nothing spins, so synchronous launches stay correct.
+    const bool split = stream >= 2 && !is_pinned(frame);
+    const int half = 1;
+    size_t in_first = in_n;
+    if (split) {
+        const int hi = std::max(w->chunk_fr_hi[half - 1], fr0);
+        in_first = std::min(in_n, size_t(hi - fr0) * frame_cols);
+    }
+    CUDA_TRY_V(cudaMemcpyAsync(d->d_frame, src, sizeof(double) * in_first, cudaMemcpyHostToDevice,
+                               d->stream));
     SolveArgs a = base_args(p, d, c, dv);
     a.frame = d->d_frame;
     a.frame_rows = frame_rows;
@@ -966,7 +988,26 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
         CUDA_TRY_V(cudaStreamWaitEvent(d->s_d2h, d->ev_h2d[2], 0));
     }
     cudaEventRecord(d->ev0, d->stream);
-    if (w->n_items > 0) {
+    if (split && w->n_items > 0) {
+        int first = 0;
+        for (int s2 = 0; s2 < half; ++s2) first += w->chunk_count[s2];
+        SolveArgs a1 = a;
+        a1.n_tasks = first;
+        if ((rc = launch(c, d, a1, d->stream, p->wt.NS))) return fail(rc);
+        // the rest of the frame on the copy stream while the first half solves
+        CUDA_TRY_V(cudaMemcpyAsync(d->d_frame + in_first, src + in_first,
+                                   sizeof(double) * (in_n - in_first), cudaMemcpyHostToDevice,
+                                   d->s_h2d));
+        CUDA_TRY_V(cudaEventRecord(d->ev_h2d[3], d->s_h2d));
+        CUDA_TRY_V(cudaStreamWaitEvent(d->stream, d->ev_h2d[3], 0));
+        SolveArgs a2 = a;
+        a2.counter = d->d_counters + (d->counter_next++ % kCounterRing);  // its own queue head
+        a2.tasks = a.tasks + first;
+        a2.task_cls = a.task_cls + first;
+        a2.n_tasks = a.n_tasks - first;
+        if ((rc = launch(c, d, a2, d->stream, p->wt.NS))) return fail(rc);
+        r->launches += 2;
+    } else if (w->n_items > 0) {
         if ((rc = launch(c, d, a, d->stream, p->wt.NS))) return fail(rc);
         r->launches += 1;
     }
@@ -978,7 +1019,7 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
             if (t.joinable()) t.join();
         }
     } joiner{prefault};
-    if (stream) prefault = prefault_async(out_band, sizeof(double) * out_n);
+    if (stream && !out_pinned) prefault = prefault_async(out_band, sizeof(double) * out_n);
     if (stream) {
         WaitValue32Fn waitv = wait_value32();
         for (int s = 0; s < stream; ++s) {
@@ -988,7 +1029,8 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
                       reinterpret_cast<CUdeviceptr>(d->d_progress + s),
                       cuuint32_t(w->chunk_count[s]), CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                 return fail(set_error(TQSB_ECUDA, "cuStreamWaitValue32 failed"));
-            if (n) cudaMemcpyAsync(d->h_out + off, d->d_out + off, sizeof(double) * n,
+            // straight into a pinned caller buffer, else into the pinned staging
+            if (n) cudaMemcpyAsync(host_out + off, d->d_out + off, sizeof(double) * n,
                                    cudaMemcpyDeviceToHost, d->s_d2h);
             cudaEventRecord(d->ev_chunk[s], d->s_d2h);
         }
@@ -1008,9 +1050,11 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
                 std::this_thread::yield();
             }
             if (q != cudaSuccess) break;
-            size_t off, n;
-            chunk_rows(s, &off, &n);
-            par_memcpy(out_band + off, d->h_out + off, sizeof(double) * n, 4);
+            if (!out_pinned) {
+                size_t off, n;
+                chunk_rows(s, &off, &n);
+                par_memcpy(out_band + off, d->h_out + off, sizeof(double) * n, 4);
+            }
         }
         if (s < stream) {  // the solve failed: unblock the waits so the copy stream drains
             const cudaError_t err = cudaStreamSynchronize(d->stream);

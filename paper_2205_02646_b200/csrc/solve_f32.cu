@@ -337,12 +337,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
                 }
             }
         }
-        if (SP) {  // streamed completion: this block's rows are final
-            __syncwarp();           // orders the lanes' stores before lane 0's release
-            if (lane == 0)
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + chunk)
-                             : "memory");
-        }
         if (tracing) {
             if (lane == 0) *a.trace_n = it;
             if (a.trace_window) {
@@ -366,17 +360,37 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         // warp-level dynamic scheduling over the class-sorted task list: no CTA-wide
         // class state (per-rank factors are read through L1), and no tail imbalance
         // beyond one block per warp
+        // streamed completion (SP): finished blocks are counted per chunk and published
+        // with one release per chunk change -- tasks come in chunk order, so a warp
+        // publishes ~once per chunk; the release orders all its earlier output stores
+        int cur_chunk = -1, pending = 0;
+        auto publish = [&]() {
+            __syncwarp();  // the lanes' stores before lane 0's release
+            if (lane == 0 && pending)
+                asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.progress + cur_chunk),
+                             "r"(pending)
+                             : "memory");
+        };
         for (;;) {
             int ti = 0;
             if (lane == 0) ti = atomicAdd(a.counter, 1);
             ti = __shfl_sync(FULL, ti, 0);
             if (ti >= a.n_tasks) break;
             const int tc = __ldg(a.task_cls + ti);
-            if constexpr (SP)
-                solve_task(ti, a.tabs[tc & ((1 << kTaskClsBits) - 1)], tc >> kTaskClsBits);
-            else
+            if constexpr (SP) {
+                const int ch = tc >> kTaskClsBits;
+                if (ch != cur_chunk) {
+                    publish();
+                    cur_chunk = ch;
+                    pending = 0;
+                }
+                solve_task(ti, a.tabs[tc & ((1 << kTaskClsBits) - 1)], ch);
+                ++pending;
+            } else {
                 solve_task(ti, a.tabs[tc], 0);
+            }
         }
+        if constexpr (SP) publish();
     } else {
         for (int it_item = blockIdx.x; it_item < a.n_items; it_item += gridDim.x) {
             const WorkItem item = a.items[it_item];
