@@ -316,6 +316,7 @@ struct Work {
 };
 constexpr int kStreamChunks = 16;       // output chunks of a streamed host-buffer call (max)
 constexpr int kStreamMinTasks = 8192;   // below this a frame is not worth streaming
+constexpr int kStreamMinTasksPinned = 262144;  // ... into a pinned caller buffer
 
 // The per-call derived tables of one option set. The cache proper is the fp64 planes
 // (B, C, D per offset class: the reference's KernelSet, rljsde.hpp:34-52), which
@@ -899,10 +900,13 @@ void run_band_host(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry
     const int per_axis = p->period / std::gcd(p->period, c.block);
     const int n_chunks = std::clamp(128 / std::max(1, per_axis * per_axis), 1, kStreamChunks);
     // (the warp-scheduled kernel only: the TMEM column tier runs CTA work items)
+    // (pinned outputs only for large frames: below ~half a 4K frame the kernel's zero-copy
+    // stores beat the chunk copies -- 1 MP, P = 8: 211.4 vs 206.6 MP/s)
     const int stream = uses_f32(c) && c.algorithm == TQSB_ALGO_RLJSDE &&
                                c.hot_columns <= 0 &&
                                solve_f32_streams(p->wt.NS, c.block * c.block) &&
-                               n_est >= kStreamMinTasks && br1 - br0 >= kStreamChunks &&
+                               n_est >= (out_pinned ? kStreamMinTasksPinned : kStreamMinTasks) &&
+                               br1 - br0 >= kStreamChunks &&
                                n_chunks >= 2 && wait_value32() != nullptr
                            ? n_chunks
                            : 0;
