@@ -86,9 +86,16 @@ def parse():
     ap.add_argument("--workload", default="4k", choices=sorted(WORKLOADS))
     ap.add_argument("--period", type=int, default=None, help="override P (HR px)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-probe", action="store_true",
+                    help="skip the FFMA2/LDS peak probe (e.g. for an ncu launch list of the step)")
     ap.add_argument("--cpu-sample-rows", type=int, default=128,
                     help="HR rows of the CPU baseline strip")
     return ap.parse_args()
+
+
+def _num(x, nd):
+    """round() for the JSON line; None for a value that was not measured (NaN)."""
+    return None if x != x else round(x, nd)
 
 
 def dist_env():
@@ -283,7 +290,8 @@ def main_ours(args):
     f0, f1 = bands.band_frame_rows(fr, W, B, br0, br1)
     out_r0, out_r1 = bands.band_output_rows(fr, B, br0, br1)
 
-    peaks = tq.probe_peaks(local)
+    peaks = (dict(fp32_tflops=float("nan"), smem_tbps=float("nan")) if args.no_probe
+             else tq.probe_peaks(local))
     plan = tq.Plan(pat, cfg, devices=[local])
     stream = torch.cuda.current_stream()
     d_frame = torch.from_numpy(frame).to(f"cuda:{local}")
@@ -475,10 +483,10 @@ def main_ours(args):
                          "peak_source": "nominal FP32 pipe: 148 SMs x 128 FMA/clk x 2 flop at "
                                         f"{nominal_mhz:.0f} MHz (the sampled max SM clock); "
                                         "MEASURED_PEAKS.json has no FP32 figure",
-                         "peak_probe": round(peaks["fp32_tflops"], 2),
-                         "probe_frac_of_nominal": round(peaks["fp32_tflops"] / peak_nominal, 4),
-                         "frac_of_probe": round(kernel_tflops / peaks["fp32_tflops"], 4),
-                         "smem_tbps_measured": round(peaks["smem_tbps"], 2),
+                         "peak_probe": _num(peaks["fp32_tflops"], 2),
+                         "probe_frac_of_nominal": _num(peaks["fp32_tflops"] / peak_nominal, 4),
+                         "frac_of_probe": _num(kernel_tflops / peaks["fp32_tflops"], 4),
+                         "smem_tbps_measured": _num(peaks["smem_tbps"], 2),
                          "executed_flop_per_block": EXEC_FLOP_BLOCK,
                          "executed_frac": round(EXEC_FLOP_BLOCK * n_blocks / (mean_ms * 1e-3)
                                                 / 1e12 / peak_nominal, 4)},
@@ -517,7 +525,8 @@ def main_video(args):
     d_outs = [torch.empty((M, N), dtype=torch.float64, device=dev) for _ in frames]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    peaks = tq.probe_peaks(local)
+    peaks = (dict(fp32_tflops=float("nan"), smem_tbps=float("nan")) if args.no_probe
+             else tq.probe_peaks(local))
     t0 = time.perf_counter()
     rep0 = plan.reconstruct_device(d_frames[0].data_ptr(), fr, fc, d_outs[0].data_ptr(), stream.cuda_stream)
     torch.cuda.synchronize()
@@ -631,7 +640,7 @@ def main_video(args):
                          "peak": round(peak_nominal, 2), "unit": "TFLOP/s",
                          "frac": round(kernel_tflops / peak_nominal, 4), "traffic": None,
                          "peak_source": "nominal FP32 pipe at the sampled max SM clock",
-                         "peak_probe": round(peaks["fp32_tflops"], 2)},
+                         "peak_probe": _num(peaks["fp32_tflops"], 2)},
             "device_stream": {"value": round(mp / (ds_mean * 1e-3), 3), "unit": "MP/s",
                               "ms_per_step": round(ds_mean, 3),
                               "includes": "synthetic scene + sensor readout + reconstruction, "

@@ -17,7 +17,7 @@ for P in 4 8 16 32; do
 done
 python bench.py --workload video --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${tag}_video.json 2> gpurun_out/${tag}_video.err
 if [ "${NCU:-1}" = 1 ]; then
-  cmd="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"
+  cmd="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-probe"
   $cmd > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/${tag}_launches.csv $cmd > gpurun_out/${tag}_ncu_list.log 2>&1
 fi
