@@ -44,6 +44,9 @@
 #ifndef TQSB_DYN
 #define TQSB_DYN 1  // warp-level dynamic task scheduling when no CTA-wide class state is needed
 #endif
+#ifndef TQSB_INIT_FFT
+#define TQSB_INIT_FFT 1  // W = 32: the init's second DFT stage as a shuffle FFT across lanes
+#endif
 #ifndef TQSB_AHEAD
 #define TQSB_AHEAD 2  // 4-slot column chunks in flight ahead of the update (NS == 16)
 #endif
@@ -144,44 +147,86 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
                 colv[eta] = v;
             }
         }
-        // step 1 (lane = gamma): Z(sigma, gamma) = sum_eta a(eta,gamma) conj(U(eta sigma))
         constexpr int H = W / 2 + 1;
-#pragma unroll
-        for (int sg = 0; sg < H; ++sg) {
-            // (zr, zi) += (a, -a) * (cos, sin): one FFMA2, the same two roundings as
-            // the scalar pair
-            float2 z = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int eta = 0; eta < W; ++eta) {
-                const float4 u = unit4[(eta * sg) % W];  // (cos, -sin, sin, -sin)
-                z = __ffma2_rn(make_float2(colv[eta], colv[eta]), make_float2(u.x, u.y), z);
-            }
-            zbuf[lane * 18 + sg] = z;
-        }
-        __syncwarp();
-        // step 2 (lane = rho): R0(sigma, rho) = sum_gamma Z(sigma,gamma) conj(U(gamma rho))
-        float2 r0[H];
-#pragma unroll
-        for (int sg = 0; sg < H; ++sg) r0[sg] = make_float2(0.f, 0.f);
-#pragma unroll 4
-        for (int g = 0; g < W; ++g) {
-            const float4 u = unit4[(g * lane) % W];
+        float2* r0buf = zbuf;
+        if constexpr (W == 32 && TQSB_INIT_FFT) {
+            // step 1 (lane = gamma): Z(sigma, gamma) = sum_eta a(eta,gamma) conj(U(eta sigma)),
+            // kept in registers
+            float2 zr[H];
 #pragma unroll
             for (int sg = 0; sg < H; ++sg) {
-                // r0 += (z.y, -z.x) * sin, then += (z.x, z.y) * cos: the scalar FMA order
-                // (inner product with sin first) as two FFMA2
-                const float2 z = zbuf[g * 18 + sg];
-                const float2 t = __ffma2_rn(make_float2(z.y, z.x), make_float2(u.z, u.w), r0[sg]);
-                r0[sg] = __ffma2_rn(z, make_float2(u.x, u.x), t);
-            }
-        }
-        __syncwarp();
-        float2* r0buf = zbuf;
-        if (lane < W) {
+                float2 z = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int sg = 0; sg < H; ++sg) r0buf[sg * W + lane] = r0[sg];
+                for (int eta = 0; eta < W; ++eta) {
+                    const float4 u = unit4[(eta * sg) % W];  // (cos, -sin, sin, -sin)
+                    z = __ffma2_rn(make_float2(colv[eta], colv[eta]), make_float2(u.x, u.y), z);
+                }
+                zr[sg] = z;
+            }
+            // step 2: R0(sigma, rho) = sum_gamma Z(sigma,gamma) conj(U(gamma rho)) as a radix-2
+            // decimation-in-frequency FFT across the lanes (lane = gamma), 5 stages of
+            // shuffle butterflies: (a, b) -> (a + b, (a - b) e^{-2 pi i j / 2h}); lane l ends
+            // with R0(sigma, bitrev(l)). 17 independent transforms per stage keep the
+            // shuffles' latency hidden; no shared-memory transpose.
+#pragma unroll
+            for (int h = 16; h >= 1; h >>= 1) {
+                const bool low = lane & h;  // holds b of its pair
+                const float2 un = unit[(lane & (h - 1)) * (16 / h)];  // (cos, sin) of the twiddle
+                const float2 sg2 = low ? make_float2(-1.f, -1.f) : make_float2(1.f, 1.f);
+                const float2 wa = low ? make_float2(un.x, un.x) : make_float2(1.f, 1.f);
+                const float2 wb = low ? make_float2(un.y, -un.y) : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int sg = 0; sg < H; ++sg) {
+                    float2 o;
+                    o.x = __shfl_xor_sync(FULL, zr[sg].x, h);
+                    o.y = __shfl_xor_sync(FULL, zr[sg].y, h);
+                    const float2 y = __ffma2_rn(sg2, zr[sg], o);        // a + b  |  a - b
+                    const float2 t = __fmul2_rn(y, wa);                    // y * w (complex)
+                    zr[sg] = __ffma2_rn(make_float2(y.y, y.x), wb, t);
+                }
+            }
+            const int rho = int(__brev(unsigned(lane)) >> 27);
+#pragma unroll
+            for (int sg = 0; sg < H; ++sg) r0buf[sg * W + rho] = zr[sg];
+            __syncwarp();
+        } else {
+            // step 1 (lane = gamma): Z(sigma, gamma) = sum_eta a(eta,gamma) conj(U(eta sigma))
+#pragma unroll
+            for (int sg = 0; sg < H; ++sg) {
+                // (zr, zi) += (a, -a) * (cos, sin): one FFMA2, the same two roundings as
+                // the scalar pair
+                float2 z = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int eta = 0; eta < W; ++eta) {
+                    const float4 u = unit4[(eta * sg) % W];  // (cos, -sin, sin, -sin)
+                    z = __ffma2_rn(make_float2(colv[eta], colv[eta]), make_float2(u.x, u.y), z);
+                }
+                zbuf[lane * 18 + sg] = z;
+            }
+            __syncwarp();
+            // step 2 (lane = rho): R0(sigma, rho) = sum_gamma Z(sigma,gamma) conj(U(gamma rho))
+            float2 r0[H];
+#pragma unroll
+            for (int sg = 0; sg < H; ++sg) r0[sg] = make_float2(0.f, 0.f);
+#pragma unroll 4
+            for (int g = 0; g < W; ++g) {
+                const float4 u = unit4[(g * lane) % W];
+#pragma unroll
+                for (int sg = 0; sg < H; ++sg) {
+                    // r0 += (z.y, -z.x) * sin, then += (z.x, z.y) * cos: the scalar FMA order
+                    // (inner product with sin first) as two FFMA2
+                    const float2 z = zbuf[g * 18 + sg];
+                    const float2 t = __ffma2_rn(make_float2(z.y, z.x), make_float2(u.z, u.w), r0[sg]);
+                    r0[sg] = __ffma2_rn(z, make_float2(u.x, u.x), t);
+                }
+            }
+            __syncwarp();
+            if (lane < W) {
+#pragma unroll
+                for (int sg = 0; sg < H; ++sg) r0buf[sg * W + lane] = r0[sg];
+            }
+            __syncwarp();
         }
-        __syncwarp();
         // gather into rank order and scale: R'_r = s_r R0[perm r]
         float4 R[NS];
 #pragma unroll
