@@ -652,10 +652,11 @@ int ensure_derived(tqsb_plan* p, Device* d, const tqsb_config& c, Derived** out,
 // the band's classes are made resident first (cached per frame shape and band).
 int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& g, int frame_rows,
                  int frame_cols, int br0, int br1, Work** out, int* created, int* launches,
-                 int stream = 0) {
+                 int stream = 0, int order_chunks = 0) {
     *created = 0;
     const int chunk = (uses_f32(c) ? kWarpsF32 : kWarpsF64) * 4;
-    const WorkKey wkey{frame_rows, frame_cols, br0, br1, g.B, chunk, stream};
+    // order_chunks: the same chunk-by-chunk order without the chunk tags (experiment knob)
+    const WorkKey wkey{frame_rows, frame_cols, br0, br1, g.B, chunk, stream > 0 ? stream : -order_chunks};
     Enumerated e;
     auto it = d->works.find(wkey);
     if (it != d->works.end()) {
@@ -690,7 +691,7 @@ int prepare_band(tqsb_plan* p, Device* d, const tqsb_config& c, const Geometry& 
     // class-sorted (stable) task list, cut into CTA work items of one class each; a
     // streamed list is ordered chunk by chunk of block rows first (class-sorted inside
     // each chunk) and carries the chunk in task_cls
-    const int n_chunks = stream > 0 ? stream : 1;
+    const int n_chunks = stream > 0 ? stream : order_chunks > 0 ? order_chunks : 1;
     const int nbr = br1 - br0;
     // chunk boundaries shrink toward the end (fraction 1 - (1 - s/S)^2): the rows handed
     // over after the kernel ends -- the exposed tail -- are the last, smallest chunk
@@ -1476,7 +1477,12 @@ int device_band(tqsb_plan* p, const tqsb_config* call, const double* d_frame, in
     Work* w = nullptr;
     Derived* dv = nullptr;
     int created = 0, launches = 0;
-    TQSB_TRY(prepare_band(p, d, c, g, frame_rows, frame_cols, br0, br1, &w, &created, &launches));
+    static const int order_env = [] {  // experiment knob: task order of the device path
+        const char* v = std::getenv("TQSB_ORDER_CHUNKS");
+        return v ? std::atoi(v) : 0;
+    }();
+    TQSB_TRY(prepare_band(p, d, c, g, frame_rows, frame_cols, br0, br1, &w, &created, &launches, 0,
+                          uses_f32(c) ? order_env : 0));
     TQSB_TRY(ensure_derived(p, d, c, &dv, &launches));
     SolveArgs a = base_args(p, d, c, dv);
     a.frame = d_frame;
