@@ -457,8 +457,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
             }
             const ClassTab ct = a.tabs[item.cls];
 
-            for (int ti = item.start + warp; ti < item.start + item.count; ti += NW)
+            for (int ti = item.start + warp; ti < item.start + item.count; ti += NW) {
+                __syncwarp();  // converged: no divergence wrapping of the solve's collectives
                 solve_task(ti, ct, 0);
+            }
         }
     }
     tmem_sync_all();
