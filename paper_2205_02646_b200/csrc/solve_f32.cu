@@ -125,8 +125,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
 
     // one target block end to end: init, nu iterations, synthesis, placement
     auto solve_task = [&](const int ti, const ClassTab& ct, const int chunk) {
+        // the class's table pointers once per task, in registers (ct refers to global
+        // memory: read inside the loop, ct.fac was re-loaded every iteration, a dependent
+        // load ahead of the step factor's own)
         const float4* __restrict__ gcols = reinterpret_cast<const float4*>(ct.cpack);
         const float2* __restrict__ scale2 = reinterpret_cast<const float2*>(ct.scale);
+        const float* __restrict__ facp = ct.fac;
+        const float* __restrict__ maskp = ct.mask32;
         const Task tk = a.tasks[ti];
         // ---------------- init: window image column per lane ----------------
         float colv[W];
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
             for (int eta = 0; eta < W; ++eta) {
                 float v = 0.f;
                 if (lane < W) {
-                    const float mk = __ldg(ct.mask32 + eta * W + lane);
+                    const float mk = __ldg(maskp + eta * W + lane);
                     int fr = (tk.origin_row + eta) >> 1;
                     fr = fr < a.frame_rows - 1 ? fr : a.frame_rows - 1;
                     const double y =
@@ -341,7 +346,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
                 for (int i = 0; i < PF; ++i) c[i] = __ldg(col + i * 32 + lane);
             }
             // (fac bits, flat k) of rank u: CTA-shared table, or through L1 when scheduled per warp
-            const int2 meta = DYN ? make_int2(__float_as_int(__ldg(ct.fac + u)), __ldg(a.wc.perm + u))
+            const int2 meta = DYN ? make_int2(__float_as_int(__ldg(facp + u)), __ldg(a.wc.perm + u))
                                   : s_meta[u];
             const float2 v = pick_elem<NS>(R, t);
             const float ure = __shfl_sync(FULL, v.x, Lw);
