@@ -25,7 +25,8 @@ def child(a):
     gt = tq.synthetic_image(a.rows, a.cols, a.seed)
     pat = tq.generate_pattern(7, a.period)
     frame = tq.simulate_measurement(gt, pat)
-    plan = tq.Plan(pat, tq.ReconstructionConfig(clip_output=False))
+    plan = tq.Plan(pat, tq.ReconstructionConfig(clip_output=False,
+                                                hot_columns=int(os.environ.get("TQSB_HOT", "-1"))))
     plan.warm(*frame.shape)
     d_frame = torch.from_numpy(frame).cuda()
     d_out = torch.empty((a.rows, a.cols), dtype=torch.float64, device="cuda")
