@@ -50,6 +50,16 @@
 #ifndef TQSB_AHEAD
 #define TQSB_AHEAD 2  // 4-slot column chunks in flight ahead of the update (NS == 16)
 #endif
+#ifndef TQSB_SMEM_PAD
+#define TQSB_SMEM_PAD 0  // experiment builds: extra shared memory (a larger carveout, less L1)
+#endif
+#ifndef TQSB_GATHER_SHARE
+// W = 32 (shuffle-FFT init): warps per half-spectrum staging buffer, taken in turns. 16 =
+// one 4.3 KB buffer per CTA: the CTA needs 5 KB of shared memory, the 8 KB carveout
+// leaves L1 248 KB for C' columns (hit rate 63 -> 74 %; 4K frame 34.53 -> 32.84 ms;
+// 1 / 2 / 4 / 8 warps per buffer: 33.80 / 33.44 / 33.10 / 32.94)
+#define TQSB_GATHER_SHARE 16
+#endif
 
 namespace tqsb {
 namespace {
@@ -59,14 +69,30 @@ using namespace dev;
 
 // per-warp scratch floats: the init transpose buffer zbuf[gamma][sigma] (float2,
 // row stride 18) / half-spectrum r0buf[sigma][rho], aliased with the element-score
-// buffer sbuf[lane][2*NS] (row stride kSbufStride floats)
+// buffer sbuf[lane][2*NS] (row stride kSbufStride floats) of the exact-selection build.
+// With the shuffle FFT and packed keys (the product path) only r0buf remains, and
+// kShare warps share one
 template <int W>
 struct Scratch {
-    static constexpr int kZ = 32 * 18 * 2;
+    static constexpr bool kFFT = W == 32 && TQSB_INIT_FFT;
+    static constexpr int kZ = kFFT ? 0 : 32 * 18 * 2;
     static constexpr int kR = (W / 2 + 1) * 32 * 2;
-    static constexpr int kS = 32 * kSbufStride;
+    static constexpr int kS = TQSB_KEYS ? 0 : 32 * kSbufStride;
     static constexpr int kFloats = (kZ > kR ? (kZ > kS ? kZ : kS) : (kR > kS ? kR : kS));
+    static constexpr int kShare = kFFT && TQSB_KEYS ? TQSB_GATHER_SHARE : 1;
+    static constexpr int buffers(int warps) { return (warps + kShare - 1) / kShare; }
 };
+
+// (fac, k) rank table in shared memory: read by the static-item schedule and the exact
+// tie scan; the dynamic schedule with packed keys reads both through L1 instead
+template <bool DYN>
+__host__ __device__ constexpr int meta_ranks(int kp) { return DYN && TQSB_KEYS ? 0 : kp; }
+
+template <int W, bool DYN>
+size_t smem_bytes(int n_slots, int warps) {
+    return size_t(meta_ranks<DYN>(n_slots * 64)) * 8 + 32 * 8 + 32 * 16 +
+           size_t(Scratch<W>::buffers(warps)) * Scratch<W>::kFloats * 4 + TQSB_SMEM_PAD;
+}
 
 // NW warps per CTA (1 CTA per SM): 16 at 128 registers where the kernel fits without
 // spilling in the loop (the default W = 32 / B = 4 product path: 38.8 vs 40.5 ms per 4K frame at 12),
@@ -81,16 +107,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
     constexpr int COLF4 = NS * 32;  // float4 per column
     constexpr int KP = NS * 64;     // padded frequency count
     constexpr int SCR = Scratch<W>::kFloats;
-    // KP x (gamma/(s_u D_u) bits, flat k) per rank u
+    // KP x (gamma/(s_u D_u) bits, flat k) per rank u (not allocated for DYN + keys)
     int2* s_meta = reinterpret_cast<int2*>(smem);
-    float2* unit = reinterpret_cast<float2*>(s_meta + KP);   // W (cos, sin)
+    float2* unit = reinterpret_cast<float2*>(s_meta + meta_ranks<DYN>(KP));   // W (cos, sin)
     float4* unit4 = reinterpret_cast<float4*>(unit + 32);    // W (cos, -sin, sin, -sin): init
     float* scr_all = reinterpret_cast<float*>(unit4 + 32);
     __shared__ int s_cls;
     __shared__ uint32_t s_tmem;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float* scr = scr_all + warp * SCR;
+    constexpr int kShare = Scratch<W>::kShare;
+    float* scr = scr_all + (warp / kShare) * SCR;
+    __shared__ int s_glock[NW];  // staging-buffer locks (kShare > 1)
+    int* glock = s_glock + warp / kShare;
+    if (threadIdx.x < NW) s_glock[threadIdx.x] = 0;
     float2* zbuf = reinterpret_cast<float2*>(scr);
     float* srow = scr + lane * kSbufStride;  // this lane's element scores
 
@@ -99,7 +129,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         unit[threadIdx.x] = make_float2(cs, sn);
         unit4[threadIdx.x] = make_float4(cs, -sn, sn, -sn);
     }
-    for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].y = a.wc.perm[r];
+    if constexpr (meta_ranks<DYN>(KP) > 0)
+        for (int r = threadIdx.x; r < KP; r += blockDim.x) s_meta[r].y = a.wc.perm[r];
     if (threadIdx.x == 0) s_cls = -1;
     // TMEM tier: a.hot columns x 4*NS TMEM columns per quadrant (512 max)
     const int hotn = TM ? a.hot : 0;  // TMEM tier (TM instantiations only)
@@ -154,7 +185,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         }
         constexpr int H = W / 2 + 1;
         float2* r0buf = zbuf;
-        if constexpr (W == 32 && TQSB_INIT_FFT) {
+        float4 R[NS];
+        if constexpr (Scratch<W>::kFFT) {
             // step 1 (lane = gamma): Z(sigma, gamma) = sum_eta a(eta,gamma) conj(U(eta sigma)),
             // kept in registers
             // with the first two radix-2 splits of a real-input FFT: U(eta sigma) repeats
@@ -207,10 +239,48 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
                     zr[sg] = __ffma2_rn(make_float2(y.y, y.x), wb, t);
                 }
             }
+            // gather into rank order and scale: R'_r = s_r R0[perm r]. The half spectrum
+            // is staged in shared memory (lane l holds column rho = bitrev(l) of every
+            // row); SHARE warps take turns on one staging buffer under a shared-memory
+            // lock held for the ~200 cycles of the gather (a task runs ~50k), so the
+            // CTA's shared memory stays small and the SM's L1 keeps the rest for C'
             const int rho = int(__brev(unsigned(lane)) >> 27);
+            const int2* __restrict__ src2 = reinterpret_cast<const int2*>(a.wc.src);
+            if constexpr (kShare > 1) {
+                // the whole warp spins on lane 0's CAS (a warp-uniform exit keeps the
+                // solve provably converged: no WARPSYNC wrapping of its collectives)
+                for (;;) {
+                    int got = 0;
+                    if (lane == 0) got = atomicCAS(glock, 0, 1) == 0;
+                    if (__shfl_sync(FULL, got, 0)) break;
+                }
+            }
 #pragma unroll
             for (int sg = 0; sg < H; ++sg) r0buf[sg * W + rho] = zr[sg];
             __syncwarp();
+#pragma unroll
+            for (int i = 0; i < NS; ++i) {
+                const int2 sp = __ldg(src2 + 32 * i + lane);  // ranks 64 i + 2 lane + {0, 1}
+                const float2 v0 = r0buf[sp.x & 0xffff], v1 = r0buf[sp.y & 0xffff];
+                R[i] = make_float4(v0.x, v1.x, v0.y, v1.y);
+            }
+            __syncwarp();
+            if constexpr (kShare > 1) {
+                if (lane == 0) {
+                    __threadfence_block();
+                    atomicExch(glock, 0);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NS; ++i) {
+                const int2 sp = __ldg(src2 + 32 * i + lane);
+                const float2 sc = __ldg(scale2 + 32 * i + lane);
+                const float im0 = (sp.x & (1 << 30)) ? -R[i].z : R[i].z;
+                const float im1 = (sp.y & (1 << 30)) ? -R[i].w : R[i].w;
+                const float2 re = __fmul2_rn(sc, make_float2(R[i].x, R[i].y));
+                const float2 im = __fmul2_rn(sc, make_float2(im0, im1));
+                R[i] = make_float4(re.x, re.y, im.x, im.y);
+            }
         } else {
             // step 1 (lane = gamma): Z(sigma, gamma) = sum_eta a(eta,gamma) conj(U(eta sigma))
 #pragma unroll
@@ -248,22 +318,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
                 for (int sg = 0; sg < H; ++sg) r0buf[sg * W + lane] = r0[sg];
             }
             __syncwarp();
-        }
-        // gather into rank order and scale: R'_r = s_r R0[perm r]
-        float4 R[NS];
+            // gather into rank order and scale: R'_r = s_r R0[perm r]
 #pragma unroll
-        for (int i = 0; i < NS; ++i) {
-            const int r = 64 * i + 2 * lane;
-            const int s0 = __ldg(a.wc.src + r), s1 = __ldg(a.wc.src + r + 1);
-            const float2 sc = __ldg(scale2 + 32 * i + lane);
-            float2 v0 = r0buf[s0 & 0xffff], v1 = r0buf[s1 & 0xffff];
-            if (s0 & (1 << 30)) v0.y = -v0.y;
-            if (s1 & (1 << 30)) v1.y = -v1.y;
-            const float2 re = __fmul2_rn(sc, make_float2(v0.x, v1.x));
-            const float2 im = __fmul2_rn(sc, make_float2(v0.y, v1.y));
-            R[i] = make_float4(re.x, re.y, im.x, im.y);
+            for (int i = 0; i < NS; ++i) {
+                const int r = 64 * i + 2 * lane;
+                const int s0 = __ldg(a.wc.src + r), s1 = __ldg(a.wc.src + r + 1);
+                const float2 sc = __ldg(scale2 + 32 * i + lane);
+                float2 v0 = r0buf[s0 & 0xffff], v1 = r0buf[s1 & 0xffff];
+                if (s0 & (1 << 30)) v0.y = -v0.y;
+                if (s1 & (1 << 30)) v1.y = -v1.y;
+                const float2 re = __fmul2_rn(sc, make_float2(v0.x, v1.x));
+                const float2 im = __fmul2_rn(sc, make_float2(v0.y, v1.y));
+                R[i] = make_float4(re.x, re.y, im.x, im.y);
+            }
+            __syncwarp();
         }
-        __syncwarp();
 #if TQSB_KEYS
         float lmax = score_pass_keys<NS>(R);
 #else
@@ -496,7 +565,8 @@ int launch_one(const SolveArgs& a, cudaStream_t stream, int num_sms) {
     // either way; it costs instructions: measured 40.6 vs 40.1 ms per 4K frame with it on)
     constexpr int NWP = PPL == 1 ? kWarpsF32 : kWarpsF32Heavy;  // product path (B <= 5)
     const int nw = (a.trace_picks || a.hot > 0) ? kWarpsF32Heavy : NWP;
-    const size_t smem = solve_f32_smem_bytes(NS, nw);
+    const bool dyn = !(a.trace_picks || a.hot > 0) && TQSB_DYN;
+    const size_t smem = dyn ? smem_bytes<W, true>(NS, nw) : smem_bytes<W, false>(NS, nw);
     auto kern = a.trace_picks ? k_solve_f32<NS, W, PPL, true, false, kWarpsF32Heavy>
                 : a.hot > 0   ? k_solve_f32<NS, W, PPL, false, true, kWarpsF32Heavy>
                               : k_solve_f32<NS, W, PPL, false, false, NWP>;
@@ -510,6 +580,10 @@ int launch_one(const SolveArgs& a, cudaStream_t stream, int num_sms) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
+#ifdef TQSB_CARVEOUT
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, TQSB_CARVEOUT);
+    if (e != cudaSuccess) return e;
+#endif
     int grid = a.n_items < num_sms ? a.n_items : num_sms;
     if (grid < 1) grid = 1;
     kern<<<grid, nw * 32, smem, stream>>>(a);
@@ -534,11 +608,6 @@ int launch_w(const SolveArgs& a, int n_slots, cudaStream_t s, int num_sms) {
 
 } // namespace
 
-
-size_t solve_f32_smem_bytes(int n_slots, int warps) {
-    // (fac, perm) per rank + unit table + per-warp scratch; hot columns live in TMEM
-    return size_t(n_slots) * 64 * 8 + 32 * 8 + 32 * 16 + size_t(warps) * Scratch<32>::kFloats * 4;
-}
 
 int solve_f32_max_hot(int n_slots, int device) {
     // TMEM tier: 512 columns per lane quadrant, 4*NS columns per C' column

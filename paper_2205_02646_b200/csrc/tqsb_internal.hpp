@@ -117,7 +117,6 @@ int launch_solve_f32(const SolveArgs& a, int n_slots, void* stream, int num_sms)
 int launch_solve_f64(const SolveArgs& a, void* stream, int num_sms);
 int launch_solve_f64r(const SolveArgs& a, void* stream, int num_sms);  // register-resident, W <= 32
 int launch_solve_ljsde(const SolveArgs& a, void* stream, int num_sms);
-size_t solve_f32_smem_bytes(int n_slots, int warps);
 int solve_f32_max_hot(int n_slots, int device);
 
 // Per-class build descriptor for the batched table kernels (tables.cu).
