@@ -1,0 +1,5 @@
+import sys,json
+for l in sys.stdin:
+    try: d=json.loads(l)
+    except Exception: print(l[:300].rstrip()); continue
+    print(d["lib"].split("/")[-1], round(d.get("min_ms",0),3), "maxabs_vs_first", d.get("max_abs_vs_first"), "psnr", d.get("psnr"))
