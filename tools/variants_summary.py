@@ -1,3 +1,7 @@
+"""One line per library from tools/variants.py output: min ms, max-abs vs the first library, PSNR.
+
+    python tools/variants.py --libs a.so b.so | python tools/variants_summary.py
+"""
 import sys,json
 for l in sys.stdin:
     try: d=json.loads(l)
