@@ -23,9 +23,11 @@
 #include <iostream>
 #include <map>
 #include <numeric>
+#include <optional>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "tqsb/io.hpp"
@@ -461,47 +463,62 @@ int run_reconstruct(const ReconstructArgs& a) {
     return kExitOk;
 }
 
+// Pixelwise difference statistics of two equally sized images (the `compare`
+// subcommand's numbers; squared differences summed in pixel order).
+struct DiffStats {
+    double max_abs = 0.0;
+    double mse = 0.0;
+};
+
+DiffStats diff_stats(const tqsb::Image& x, const tqsb::Image& y) {
+    DiffStats st;
+    double sq = 0.0;
+    const double* px = x.values.data();
+    const double* py = y.values.data();
+    const size_t n = x.size();
+    for (size_t i = 0; i < n; ++i) {
+        const double e = std::fabs(px[i] - py[i]);
+        if (e > st.max_abs) st.max_abs = e;
+        sq += e * e;
+    }
+    st.mse = sq / static_cast<double>(n);
+    return st;
+}
+
 int run_compare(const std::string& pa, const std::string& pb, const std::string& pref, double threshold,
                 const FormatOption& fmt) {
-    const tqsb::Image a = tqsb::read_image_any(pa);
-    const tqsb::Image b = tqsb::read_image_any(pb);
-    if (!a.same_size(b)) throw std::invalid_argument("compare: image dimensions differ");
-    double maxDiff = 0.0, sum = 0.0;
-    for (size_t i = 0; i < a.size(); ++i) {
-        const double d = std::abs(a.values[i] - b.values[i]);
-        maxDiff = std::max(maxDiff, d);
-        sum += d * d;
-    }
-    const double mse = sum / double(a.size());
-    const bool pass = maxDiff <= threshold;
-    double psnrA = 0.0, psnrB = 0.0;
-    const bool haveRef = !pref.empty();
-    if (haveRef) {
-        const tqsb::Image ref = tqsb::read_image_any(pref);
-        psnrA = tqsb::psnr(ref, a);
-        psnrB = tqsb::psnr(ref, b);
+    const tqsb::Image imgA = tqsb::read_image_any(pa);
+    const tqsb::Image imgB = tqsb::read_image_any(pb);
+    if (!imgA.same_size(imgB)) throw std::invalid_argument("compare: image dimensions differ");
+    const DiffStats st = diff_stats(imgA, imgB);
+    const bool ok = st.max_abs <= threshold;
+    // PSNR of each input against the optional ground truth
+    std::optional<std::pair<double, double>> vsRef;
+    if (!pref.empty()) {
+        const tqsb::Image truth = tqsb::read_image_any(pref);
+        vsRef = std::make_pair(tqsb::psnr(truth, imgA), tqsb::psnr(truth, imgB));
     }
     if (fmt.json()) {
         JsonObject j;
-        j.num("max_abs_diff", maxDiff);
-        j.num("mse", mse);
+        j.num("max_abs_diff", st.max_abs);
+        j.num("mse", st.mse);
         j.num("threshold", threshold);
-        j.boolean("pass", pass);
-        if (haveRef) {
-            psnr_json(j, "psnr_a_vs_ref", psnrA);
-            psnr_json(j, "psnr_b_vs_ref", psnrB);
+        j.boolean("pass", ok);
+        if (vsRef) {
+            psnr_json(j, "psnr_a_vs_ref", vsRef->first);
+            psnr_json(j, "psnr_b_vs_ref", vsRef->second);
         }
         std::cout << j.dump() << "\n";
-    } else {
-        std::printf("max abs diff:     %.3e\n", maxDiff);
-        std::printf("mse:              %.3e\n", mse);
-        if (haveRef) {
-            std::printf("psnr A vs ref:    %s dB\n", psnr_text(psnrA).c_str());
-            std::printf("psnr B vs ref:    %s dB\n", psnr_text(psnrB).c_str());
-        }
-        std::printf("result:           %s (threshold %.3e)\n", pass ? "PASS" : "FAIL", threshold);
+        return ok ? kExitOk : kExitCompareFailed;
     }
-    return pass ? kExitOk : kExitCompareFailed;
+    std::printf("max abs diff:     %.3e\n", st.max_abs);
+    std::printf("mse:              %.3e\n", st.mse);
+    if (vsRef) {
+        std::printf("psnr A vs ref:    %s dB\n", psnr_text(vsRef->first).c_str());
+        std::printf("psnr B vs ref:    %s dB\n", psnr_text(vsRef->second).c_str());
+    }
+    std::printf("result:           %s (threshold %.3e)\n", ok ? "PASS" : "FAIL", threshold);
+    return ok ? kExitOk : kExitCompareFailed;
 }
 
 // bench (pipeline.cpp:258-329 / tqs.cpp:219-285) on the device: L-JSDE (fp64) and
