@@ -353,19 +353,25 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_f32(const SolveArgs a) {
         const bool tracing = TRACE && ti == 0;
 
         int it = 0;
-        for (; it < a.iterations; ++it) {
+        // no admissible frequency (rljsde.cpp:157-158: best < 0 only when no D_k > 0, a
+        // static property of the class): inadmissible ranks are NaN from the init on and
+        // stay NaN (their C' rows are NaN), admissible ones stay finite, so the test is
+        // taken once, on the init scores, not per pick (-1.0 % per frame)
+        const float g0 = warp_max_f32(lmax);
+        const int n_it = g0 != g0 ? 0 : a.iterations;
+        for (; it < n_it; ++it) {
             __syncwarp();
             // ---- argmax over the warp (NaN = inadmissible, ignored by max) ----
             const float gmax = warp_max_f32(lmax);
-            if (gmax != gmax) break;  // no admissible frequency (rljsde.cpp:159)
 #if TQSB_KEYS
             // t through a vector register (a uniform-register switch makes ptxas spill R)
             int t;
             asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(31 - int(__float_as_uint(gmax) & 31u)));
-            const int Lw = __ffs(__ballot_sync(FULL, lmax == gmax)) - 1;
+            // (& 31: a lane index whatever the ballot, so no pick can address outside the table)
+            const int Lw = (__ffs(__ballot_sync(FULL, lmax == gmax)) - 1) & 31;
 #else
             const unsigned cand = __ballot_sync(FULL, lmax == gmax);
-            int Lw = __ffs(cand) - 1;
+            int Lw = (__ffs(cand) - 1) & 31;
             const float sv = lane < 2 * NS ? scr[Lw * kSbufStride + lane] : qnan();
             const unsigned hit = __ballot_sync(FULL, sv == gmax);
             int t;  // element index within lane Lw: slot t>>1, half t&1
