@@ -297,6 +297,11 @@ __device__ __forceinline__ float update_uni(float4 (&R)[NS], float4 (&c)[NS], bo
         R[i] = make_float4(re.x, re.y, im.x, im.y);
         const float2 sc = __ffma2_rn(im, im, __fmul2_rn(re, re));
         if constexpr (KEYS) {
+            if (i == NS - 1)  // the last slot's keys enter at the final level: one FMNMX3
+                              // less between the last update and the warp max (the max of
+                              // the same set, NaN-ignoring: bitwise the same key)
+                return fmax3(fmax3(fmax3(m4[0], m4[1], m4[2]), m4[3], qnan()),
+                             score_key(sc.x, 2 * i, kmask), score_key(sc.y, 2 * i + 1, kmask));
             m4[i & 3] = fmax3(m4[i & 3], score_key(sc.x, 2 * i, kmask), score_key(sc.y, 2 * i + 1, kmask));
         } else {
             m4[i & 3] = fmax3(m4[i & 3], sc.x, sc.y);
